@@ -1,0 +1,370 @@
+"""Pins for the oracle (SURVEY §8(c) "What pins each part").  CPU only.
+
+Each test fixes the oracle to something other than itself: a value the paper prints or
+that Eq. (1) gives in closed form at special angles, an invariant, a textbook dense
+construction, or brute-force enumeration of the network.  A plausible mistake (a dropped
+term, a sign, a transposed U[out][in], a wrong bit order, a projector on the wrong wire
+segment) fails at least one of them (see the comment on each test).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from tn_inputs import circuits as cc
+from tn_inputs import bitstrings as bs
+from tn_inputs import configs
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def small_circuit(rows, cols, cycles, seed, seq="ABCDCDAB", final=True):
+    return cc.generate_circuit(cc.rect_layout(rows, cols), cycles, seq, seed, final)
+
+
+def load_golden_fsim():
+    U = np.zeros((4, 4), complex)
+    for line in open(os.path.join(GOLD, "fsim_theta_pi2_phi_pi6.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        r, c, re, im = line.split()
+        U[int(r), int(c)] = float(re) + 1j * float(im)
+    return U
+
+
+# --------------------------------------------------------------------------- gates
+
+def test_fsim_special_angles(oracle_built):
+    """Eq. (1) at theta=pi/2, phi=pi/6 (golden, worked by hand) and fSim(0,0) = I.
+    Catches a wrong sign of -i sin, a swapped e^{-i phi} conjugation, misplaced entries."""
+    from oracle import sv
+    np.testing.assert_allclose(sv.fsim_matrix(math.pi / 2, math.pi / 6), load_golden_fsim(), atol=1e-15)
+    np.testing.assert_allclose(sv.fsim_matrix(0.0, 0.0), np.eye(4), atol=1e-15)
+
+
+def test_fsim_unitary(oracle_built):
+    from oracle import sv
+    r = np.random.default_rng(1)
+    for _ in range(50):
+        U = sv.fsim_matrix(*r.uniform(-3, 3, 2))
+        assert np.abs(U.conj().T @ U - np.eye(4)).max() < 1e-12
+
+
+def test_pinned_fsim_singular_values(oracle_built):
+    """pinning one input of fSim gives squared singular values
+    {1+sin^2 t, cos^2 t}; at t = pi/3 these are {1.75, 0.25} (golden).  All four pinning cases.
+    Pins the magnitudes and positions of the cos/sin entries of the oracle's Eq. (1)."""
+    from oracle import sv
+    vals = open(os.path.join(GOLD, "pinned_fsim_singular_values.txt")).read().split("squared_singular_values")[1].split()
+    want = sorted(map(float, vals), reverse=True)
+    for theta, phi, expect in [(math.pi / 3, 0.7, want)] + [
+            (t, p, [1 + math.sin(t) ** 2, math.cos(t) ** 2]) for t, p in np.random.default_rng(2).uniform(0, 3, (20, 2))]:
+        U = sv.fsim_matrix(theta, phi)          # U[out=(oa,ob)][in=(ia,ib)]
+        T = U.reshape(2, 2, 2, 2)               # [oa, ob, ia, ib]
+        for which in ("ia", "ib"):
+            for v in (0, 1):
+                E = T[:, :, v, :] if which == "ia" else T[:, :, :, v]   # [oa, ob, other_in]
+                # L323/L333: group (pinned input, other input, one output) against the companion
+                # output omega, which is the output of the OTHER qubit (ob when ia is pinned,
+                # oa after "swapping the third and the fourth dimension" when ib is pinned)
+                comp = 1 if which == "ia" else 0
+                F = np.moveaxis(E, comp, -1).reshape(4, 2)
+                s2 = np.sort(np.linalg.svd(F, compute_uv=False) ** 2)[::-1]
+                np.testing.assert_allclose(s2, sorted(expect, reverse=True), atol=1e-12)
+
+
+# --------------------------------------------------------------------------- state vector
+
+def kron_reference(circuit):
+    """Textbook construction (n <= 6): each gate as a full 2^n x 2^n matrix, psi = prod M_g e_0.
+    Uses tn_brute's independent Eq. (1).  Qubit 0 = MSB; U[out][in]; fSim local index 2*x_a+x_b."""
+    from oracle.tn_brute import fsim
+    n = circuit["n"]
+    N = 1 << n
+    psi = np.zeros(N, complex)
+    psi[0] = 1
+    for g in cc.gate_list(circuit):
+        M = np.zeros((N, N), complex)
+        if g["type"] == "single":
+            q = g["target"]
+            ops = [np.eye(2)] * n
+            ops = list(ops)
+            ops[q] = np.asarray(g["matrix"], complex)
+            M = ops[0]
+            for o in ops[1:]:
+                M = np.kron(M, o)
+        else:
+            a, b = g["targets"]
+            U = fsim(g["theta"], g["phi"])
+            ma, mb = 1 << (n - 1 - a), 1 << (n - 1 - b)
+            for i in range(N):
+                for o in range(N):
+                    if (i & ~(ma | mb)) != (o & ~(ma | mb)):
+                        continue
+                    li = 2 * bool(i & ma) + bool(i & mb)
+                    lo = 2 * bool(o & ma) + bool(o & mb)
+                    M[o, i] = U[lo, li]
+        psi = M @ psi
+    return psi
+
+
+@pytest.mark.parametrize("shape,cycles,seed", [((2, 2), 3, 11), ((2, 3), 4, 12), ((1, 5), 5, 13), ((2, 3), 6, 14)])
+def test_statevector_matches_kron(oracle_built, shape, cycles, seed):
+    """Catches transposed U[out][in] (sqrtY/sqrtW are not symmetric), LSB/MSB bit order, and the
+    2*x_a + x_b local index of the fSim."""
+    from oracle import sv
+    c = small_circuit(*shape, cycles, seed)
+    np.testing.assert_allclose(sv.statevector(c), kron_reference(c), atol=1e-12)
+
+
+def test_statevector_norm(oracle_built):
+    from oracle import sv
+    for seed in range(5):
+        psi = sv.statevector(small_circuit(3, 4, 6, 100 + seed))
+        assert abs(np.vdot(psi, psi).real - 1) < 1e-12
+
+
+def test_product_state_closed_form(oracle_built):
+    """Single-qubit-only circuit: psi = kron_q (U_q,last ... U_q,1 |0>)."""
+    from oracle import sv
+    c = cc.generate_circuit(cc.rect_layout(1, 5), 0, "A", 7, final_layer=True)
+    c["moments"] += cc.generate_circuit(cc.rect_layout(1, 5), 0, "A", 8, final_layer=True)["moments"]
+    per_q = []
+    for q in range(5):
+        v = np.array([1, 0], complex)
+        for g in cc.gate_list(c):
+            if g["target"] == q:
+                v = np.asarray(g["matrix"], complex) @ v
+        per_q.append(v)
+    want = per_q[0]
+    for v in per_q[1:]:
+        want = np.kron(want, v)
+    np.testing.assert_allclose(sv.statevector(c), want, atol=1e-14)
+
+
+def test_single_fsim_on_00(oracle_built):
+    """a single fSim on |00> gives the first column of Eq. (1) = e_0."""
+    from oracle import sv
+    c = {"n": 2, "moments": [[{"type": "fsim", "targets": [0, 1], "theta": 1.1, "phi": 0.4}]]}
+    np.testing.assert_allclose(sv.statevector(c), [1, 0, 0, 0], atol=1e-15)
+
+
+# --------------------------------------------------------------------------- brute-force network
+
+@pytest.mark.parametrize("shape,cycles,seed,nfix", [((2, 2), 2, 21, 0), ((2, 2), 3, 22, 2), ((1, 3), 3, 23, 3),
+                                                     ((2, 2), 2, 24, 4)])
+def test_statevector_matches_bruteforce_network(oracle_built, shape, cycles, seed, nfix):
+    """O6: the network evaluated by definition (sum over internal wire values of products of gate
+    entries) equals the state vector; with sliced wires fixed to v it equals the state vector
+    with Pi_v inserted after the k-th gate on q (pins the wire-segment convention of App. A.2)."""
+    from oracle import sv, tn_brute
+    c = small_circuit(*shape, cycles, seed)
+    wires, _ = tn_brute.internal_wires(c)
+    r = np.random.default_rng(seed)
+    pick = [wires[i] for i in r.choice(len(wires), size=nfix, replace=False)] if nfix else []
+    vals = list(r.integers(0, 2, size=nfix))
+    fixed = {w: int(v) for w, v in zip(pick, vals)}
+    psi = sv.statevector(c, [(q, k, v) for (q, k), v in fixed.items()])
+    n = c["n"]
+    for x in range(1 << n):
+        assert abs(tn_brute.amplitude(c, x, fixed) - psi[x]) < 1e-12
+
+
+# --------------------------------------------------------------------------- slicing identities
+
+def fsim_wires(circuit):
+    """(q,k) right after each fSim (the wire segments a simplified network can slice)."""
+    n = circuit["n"]
+    count = [0] * n
+    out = []
+    gl = cc.gate_list(circuit)
+    tot = [0] * n
+    for g in gl:
+        for q in ([g["target"]] if g["type"] == "single" else g["targets"]):
+            tot[q] += 1
+    for g in gl:
+        qs = [g["target"]] if g["type"] == "single" else g["targets"]
+        for q in qs:
+            count[q] += 1
+            if g["type"] == "fsim" and count[q] < tot[q]:
+                out.append((q, count[q]))
+    return out
+
+
+def test_sum_over_all_slices_is_unsliced(oracle_built):
+    """the sum of all sub-task results returns the original contraction."""
+    from oracle import sv
+    c = small_circuit(3, 3, 6, 31)
+    W = fsim_wires(c)
+    r = np.random.default_rng(3)
+    wires = [W[i] for i in r.choice(len(W), 4, replace=False)]
+    x = np.arange(1 << c["n"], dtype=np.uint64)
+    full, _ = sv.amplitudes(c, x)
+    tot = sv.sliced_amplitudes(c, x, wires, range(16))
+    np.testing.assert_allclose(tot, full, atol=1e-12)
+
+
+def test_prefix_equals_pinned(oracle_built):
+    """S = [0, 2^(s-j)) equals Pi_0 on w_0..w_{j-1} only."""
+    from oracle import sv
+    c = small_circuit(3, 3, 6, 32)
+    W = fsim_wires(c)
+    wires = W[3:8]
+    x = np.arange(1 << c["n"], dtype=np.uint64)
+    s = len(wires)
+    for j in range(s + 1):
+        a, _ = sv.prefix_amplitudes(c, x, wires, j)
+        b = sv.sliced_amplitudes(c, x, wires, range(1 << (s - j)))
+        np.testing.assert_allclose(a, b, atol=1e-12)
+
+
+def test_edge_breaking_pauli_split(oracle_built):
+    """E = (1,0)x(1,0) = I/2 + sigma_z/2, so psi_{Pi_0} = psi/2 + psi_{sigma_z}/2."""
+    from oracle import sv
+    c = small_circuit(3, 3, 5, 33)
+    for (q, k) in fsim_wires(c)[:6]:
+        p0 = sv.statevector(c, [(q, k, 0)])
+        pz = sv.statevector(c, [(q, k, 2)])
+        np.testing.assert_allclose(p0, 0.5 * sv.statevector(c) + 0.5 * pz, atol=1e-13)
+
+
+def test_slices_orthogonal_on_latest_wire(oracle_built):
+    """SURVEY §8(c) item 11 (derived from PAPER.md L248): <psi_s|psi_t> = 0 exactly when s, t
+    differ on the latest sliced wire (U^dag U cancels after it; Pi_a Pi_b = delta_ab Pi_a)."""
+    from oracle import sv
+    c = small_circuit(3, 3, 6, 34)
+    W = fsim_wires(c)
+    gl_index = {}
+    # order wires by time: the wire list is produced in circuit order already
+    early, late = W[2], W[-3]
+    wires = [early, late]
+    psis = [sv.statevector(c, sv.slice_insertions(wires, s)) for s in range(4)]
+    # sigma bit1 (LSB) = late wire value
+    assert abs(np.vdot(psis[0], psis[1])) < 1e-13
+    assert abs(np.vdot(psis[2], psis[3])) < 1e-13
+    assert abs(np.vdot(psis[0], psis[3])) < 1e-13
+
+
+# --------------------------------------------------------------------------- rows (O7)
+
+def test_paper_three_qubit_example():
+    """request {111, 010, 000}; merging qubits 2 and 3 needs only {11, 10, 00}."""
+    from oracle import rows
+    lines = dict(l.split(None, 1) for l in open(os.path.join(GOLD, "paper_3qubit_example.txt"))
+                 if l.strip() and not l.startswith("#"))
+    req = np.array([int(s, 2) for s in lines["request"].split()], np.uint64)
+    Q = [int(t) for t in lines["merged_qubits"].split()]
+    got = rows.rows(req, 3, Q)
+    assert [format(int(v), "02b") for v in got] == lines["rows"].split()
+    assert [format(int(v), "03b") for v in rows.rows(req, 3, [0, 1, 2])] == lines["final_rows"].split()
+
+
+def test_rows_full_request_is_dense():
+    """request = all 2^n bitstrings degenerates to the dense case."""
+    from oracle import rows
+    n = 6
+    x = bs.all_bitstrings(n)
+    for Q in ([0], [1, 4], [0, 2, 3, 5]):
+        np.testing.assert_array_equal(rows.rows(x, n, Q), np.arange(1 << len(Q)))
+
+
+def test_parent_map_bruteforce():
+    from oracle import rows
+    n = 10
+    x = bs.generate_groups(n, [8, 9], 40, 5)
+    Qc, Qp = [1, 3, 4, 7], [3, 7]
+    rc = rows.rows(x, n, Qc)
+    rp = rows.rows(x, n, Qp)
+    pm = rows.parent_map(x, n, Qc, Qp)
+    for r, p in zip(rc, pm):
+        bits = {q: (int(r) >> (len(Qc) - 1 - i)) & 1 for i, q in enumerate(Qc)}
+        key = 0
+        for q in Qp:
+            key = 2 * key + bits[q]
+        assert int(rp[p]) == key
+
+
+# --------------------------------------------------------------------------- metrics / sampler
+
+def test_fidelity_definitions(oracle_built):
+    from oracle import metrics, sv
+    psi = sv.statevector(small_circuit(2, 3, 5, 41))
+    assert abs(metrics.f_exact(psi, psi) - 1) < 1e-12
+    assert abs(metrics.f_exact(psi, np.exp(0.7j) * 3 * psi) - 1) < 1e-12     # phase/scale invariant
+    orth = np.zeros_like(psi)
+    i = np.argmax(np.abs(psi))
+    orth[i] = -np.conj(psi[(i + 1) % len(psi)])
+    orth[(i + 1) % len(psi)] = np.conj(psi[i])
+    assert metrics.f_exact(psi, orth) < 1e-25
+    assert abs(metrics.f_norm(psi, 6) - 1) < 1e-12                            # full request, exact state
+
+
+def test_xeb_uniform_and_exact(oracle_built):
+    """F_XEB = (2^n/L) sum P(s_i) - 1: ~1 for exact samples of a Porter-Thomas
+    state, ~0 for uniform samples."""
+    from oracle import metrics, sv
+    c = small_circuit(3, 4, 12, 42)
+    n = c["n"]
+    p = np.abs(sv.statevector(c)) ** 2
+    r = np.random.default_rng(0)
+    L = 1 << 15
+    exact = r.choice(len(p), size=L, p=p / p.sum())
+    unif = r.integers(0, len(p), size=L)
+    assert abs(metrics.linear_xeb(p[exact], n) - 1) < 0.1
+    assert abs(metrics.linear_xeb(p[unif], n)) < 0.05
+
+
+def test_sampler_distribution():
+    """Categorical within a group: empirical frequencies match |a|^2 / sum (chi^2), one
+    non-zero amplitude is always drawn, l = 1 draws the only bitstring."""
+    from oracle import metrics
+    l = 8
+    r = np.random.default_rng(5)
+    a = (r.normal(size=l) + 1j * r.normal(size=l)).astype(np.complex64)
+    p = np.abs(a.astype(complex)) ** 2
+    p /= p.sum()
+    G = 20000
+    amps = np.tile(a, G)
+    picks = metrics.sample_groups(amps, l, seed=123) % l
+    cnt = np.bincount(picks, minlength=l)
+    chi2 = ((cnt - G * p) ** 2 / (G * p)).sum()
+    assert chi2 < 30  # 7 dof, p ~ 1e-4
+    one = np.zeros(l, np.complex64)
+    one[5] = 0.3
+    assert set(metrics.sample_groups(np.tile(one, 50), l, 9) % l) == {5}
+    np.testing.assert_array_equal(metrics.sample_groups(a, 1, 3), np.arange(l))
+
+
+@pytest.mark.parametrize("seed", [51, 52, 53, 54, 55, 56])
+def test_one_broken_edge_halves_fidelity(oracle_built, seed):
+    """breaking an edge (Pi_0 insertion) mid-circuit gives F ~ 1/2
+    (statistical; checked on the ensemble mean below with a loose per-circuit bound)."""
+    from oracle import metrics, sv
+    c = small_circuit(3, 4, 10, seed)
+    W = fsim_wires(c)
+    mid = W[len(W) // 2]
+    F = metrics.f_exact(sv.statevector(c), sv.statevector(c, [(mid[0], mid[1], 0)]))
+    assert 0.25 < F < 0.75
+
+
+def test_porter_thomas(oracle_built):
+    """deep random circuits are Porter-Thomas: 2^n p ~ Exp(1) (KS statistic)."""
+    from oracle import sv
+    c = small_circuit(4, 4, 14, 61)
+    N = 1 << c["n"]
+    x = np.sort(N * np.abs(sv.statevector(c)) ** 2)
+    ecdf = np.arange(1, N + 1) / N
+    ks = np.max(np.abs(ecdf - (1 - np.exp(-x))))
+    assert ks < 0.02
+
+
+def test_config_structure():
+    """Generator structure."""
+    s = cc.sycamore_sites()
+    assert len(s) == 54 and len(cc.couplers(s)) == 88
+    l53 = cc.sycamore53_layout()
+    assert len(l53) == 53 and len(cc.couplers(l53)) == 86
+    assert [cc.count_fsim(configs.get(k).circuit()) for k in (1, 2, 3, 4, 5)] == [17, 62, 147, 301, 430]
+    b = configs.get(2).bitstrings(20)
+    assert len(b) == 4096 and len(np.unique(b)) == 4096
