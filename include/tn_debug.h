@@ -1,0 +1,28 @@
+/*
+ * tn_debug.h -- diagnostic entry points of the same library (unit tests and benchmarks only).
+ * Not part of the method's call sequence (see tn.h).
+ */
+#ifndef TN_B200_DEBUG_H
+#define TN_B200_DEBUG_H
+
+#include "tn.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* C[M][N] = A[M][K] * B[K][N] for complex64 row-major DEVICE buffers through the tensor-core path of
+ * tn_contract (3xTF32 split pre-passes + the tcgen05 GEMM).  N >= 64 and K >= 16
+ * must be powers of two; M is arbitrary (ragged last tile).  Synchronises cuda_stream.  EINVAL on bad
+ * shapes, ECUDA on a CUDA failure. */
+tn_status tn_debug_gemm_tf32x3(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
+                               void* cuda_stream);
+
+/* Size of the simplified network built by tn_build: alive tensors, all edges, internal
+ * (sliceable) edges. */
+tn_status tn_debug_network(const tn_ctx* ctx, int64_t* n_tensors, int64_t* n_edges, int64_t* n_internal);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,315 @@
+// api.cpp -- the extern "C" boundary declared in include/tn.h and include/tn_debug.h.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <sstream>
+#include <string>
+
+#include "../../include/tn_debug.h"
+#include "exec.h"
+#include "tnb.h"
+
+struct tn_ctx {
+    std::string err;
+    tnb::Network net;
+    tnb::Request req;
+    std::vector<tnb::Leaf> leaves;
+    bool planned = false;
+    tnb::Plan plan;
+    tnb::Program prog;
+    std::vector<int32_t> sliced_wires;
+    tn_plan_info info{};
+    tnb::Device* dev = nullptr;
+};
+
+namespace {
+
+tn_status fail(tn_ctx* c, tn_status s, const std::string& m) {
+    if (c) c->err = m;
+    return s;
+}
+
+// splitmix64 counter-based stream (identical definition in tn_inputs/rng.py)
+inline uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+inline uint64_t rng_key(uint64_t seed, uint64_t tag) { return mix64(seed ^ (tag * 0xD1B54A32D192ED03ull)); }
+inline uint64_t rng_word(uint64_t key, uint64_t i) { return mix64(key + (i + 1) * 0x9E3779B97F4A7C15ull); }
+constexpr uint64_t TAG_SAMPLER = 4;
+
+}  // namespace
+
+extern "C" {
+
+const char* tn_version(void) { return "tnb200 0.1 (sm_100a)"; }
+
+const char* tn_last_error(const tn_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+void tn_destroy(tn_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->dev) tnb::dev_destroy(ctx->dev);
+    delete ctx;
+}
+
+tn_status tn_build(const tn_circuit* circuit, const uint64_t* bitstrings, int64_t M, uint64_t open_mask,
+                   tn_ctx** out) {
+    if (!out) return TN_EINVAL;
+    *out = nullptr;
+    tn_ctx* c = new tn_ctx();
+    *out = c;  // returned even on failure so that tn_last_error works; caller must tn_destroy
+    if (!circuit || !bitstrings || M < 1) return fail(c, TN_EINVAL, "null circuit/bitstrings or M < 1");
+    const int n = circuit->n_qubits;
+    if (n < 1 || n > 63) return fail(c, TN_EINVAL, "n_qubits must be in [1, 63]");
+    const uint64_t full = (n == 64) ? ~0ull : ((1ull << n) - 1);
+    if (open_mask & ~full) return fail(c, TN_EINVAL, "open_mask has bits outside the n qubits");
+    tnb::Request& r = c->req;
+    r.n = n;
+    r.open_mask = open_mask;
+    r.M = M;
+    r.bits.assign(bitstrings, bitstrings + M);
+    for (int64_t j = 0; j < M; j++)
+        if (r.bits[j] & ~full) {
+            std::ostringstream o;
+            o << "bitstring " << j << " has bits beyond the " << n << " qubits";
+            return fail(c, TN_EINVAL, o.str());
+        }
+    const int nopen = __builtin_popcountll(open_mask);
+    r.l = (int64_t)1 << nopen;
+    if (M % r.l) return fail(c, TN_EINVAL, "M is not a multiple of l = 2^popcount(open_mask)");
+    r.L = M / r.l;
+    if (open_mask) {
+        // open configuration mu -> its bits, lowest open qubit id = MSB of mu
+        std::vector<int> oq;
+        for (int q = 0; q < n; q++)
+            if ((open_mask >> (n - 1 - q)) & 1) oq.push_back(q);
+        for (int64_t g = 0; g < r.L; g++) {
+            const uint64_t f = r.bits[g * r.l] & ~open_mask;
+            for (int64_t mu = 0; mu < r.l; mu++) {
+                uint64_t want = f;
+                for (int i = 0; i < nopen; i++)
+                    if ((mu >> (nopen - 1 - i)) & 1) want |= 1ull << (n - 1 - oq[i]);
+                if (r.bits[g * r.l + mu] != want) {
+                    std::ostringstream o;
+                    o << "group " << g << " entry " << mu << " breaks the group structure (shared fixed bits, "
+                      << "open bits ascending)";
+                    return fail(c, TN_EINVAL, o.str());
+                }
+            }
+        }
+    }
+    r.fixed.resize(M);
+    for (int64_t j = 0; j < M; j++) r.fixed[j] = r.bits[j] & ~open_mask;
+    std::sort(r.fixed.begin(), r.fixed.end());
+    r.fixed.erase(std::unique(r.fixed.begin(), r.fixed.end()), r.fixed.end());
+
+    std::string e = tnb::build_network(circuit, c->net);
+    if (!e.empty()) return fail(c, TN_EINVAL, e);
+    for (auto& E : c->net.edges)
+        if (E.output && ((open_mask >> (n - 1 - E.q)) & 1)) E.open = true;
+    tnb::simplify(c->net);
+    c->leaves = tnb::make_leaves(c->net, r);
+    return TN_OK;
+}
+
+tn_status tn_plan(tn_ctx* ctx, const tn_slicing* slicing, int64_t max_tensor_size, tn_plan_info* info) {
+    if (!ctx) return TN_EINVAL;
+    if (ctx->leaves.empty()) return fail(ctx, TN_EINVAL, "tn_plan before a successful tn_build");
+    if (max_tensor_size < 1) return fail(ctx, TN_EINVAL, "max_tensor_size must be >= 1");
+    if (max_tensor_size > (1ll << 32)) return fail(ctx, TN_EINVAL, "max_tensor_size must be <= 2^32");
+    if (ctx->dev) {
+        tnb::dev_destroy(ctx->dev);
+        ctx->dev = nullptr;
+    }
+    tnb::PlanOptions opt;
+    opt.max_elems = (double)max_tensor_size;
+    if (slicing) {
+        opt.n_sliced = slicing->n_sliced;
+        opt.seed = slicing->seed;
+        opt.trials = slicing->trials;
+        opt.time_budget_s = slicing->time_budget_s;
+        if (slicing->n_forced < 0 || (slicing->n_forced > 0 && !slicing->forced_wires))
+            return fail(ctx, TN_EINVAL, "bad forced wires");
+        for (int i = 0; i < slicing->n_forced; i++) {
+            int q = slicing->forced_wires[2 * i], k = slicing->forced_wires[2 * i + 1];
+            int found = -1;
+            for (int e = 0; e < (int)ctx->net.edges.size(); e++) {
+                const tnb::Edge& E = ctx->net.edges[e];
+                if (E.q == q && E.k == k && !E.output && E.t1 >= 0 && ctx->net.tensors[E.t0].alive &&
+                    ctx->net.tensors[E.t1].alive)
+                    found = e;
+            }
+            if (found < 0) {
+                std::ostringstream o;
+                o << "forced wire (" << q << "," << k << ") is not a sliceable edge of the simplified network";
+                return fail(ctx, TN_EINVAL, o.str());
+            }
+            if (std::find(opt.forced.begin(), opt.forced.end(), found) != opt.forced.end())
+                return fail(ctx, TN_EINVAL, "duplicate forced wire");
+            opt.forced.push_back(found);
+        }
+        if (opt.n_sliced >= 0 && opt.n_sliced < (int)opt.forced.size())
+            return fail(ctx, TN_EINVAL, "n_sliced smaller than the number of forced wires");
+        if (opt.n_sliced > 62) return fail(ctx, TN_EINVAL, "n_sliced must be <= 62");
+    }
+    tnb::Plan plan;
+    std::string e = tnb::find_plan(ctx->net, ctx->leaves, ctx->req, opt, plan);
+    if (!e.empty()) return fail(ctx, TN_EINFEASIBLE, e);
+    e = tnb::lower_plan(ctx->net, ctx->leaves, ctx->req, plan, ctx->prog);
+    if (!e.empty()) return fail(ctx, TN_EINVAL, e);
+    ctx->plan = plan;
+    ctx->planned = true;
+    ctx->sliced_wires.clear();
+    for (int eid : plan.sliced) {
+        ctx->sliced_wires.push_back(ctx->net.edges[eid].q);
+        ctx->sliced_wires.push_back(ctx->net.edges[eid].k);
+    }
+    tn_plan_info& I = ctx->info;
+    I = tn_plan_info{};
+    I.s = (int32_t)plan.sliced.size();
+    I.sliced_wires = ctx->sliced_wires.data();
+    I.n_tensors = (int64_t)ctx->leaves.size();
+    I.n_steps = ctx->prog.n_pairs;
+    I.n_launches = (int64_t)ctx->prog.steps.size();
+    I.peak_elems = std::max<int64_t>(ctx->prog.peak_elems, 1);
+    I.workspace_bytes = ctx->prog.work_bytes;
+    I.cmac_per_slice = ctx->prog.cmac;
+    I.bytes_per_slice = ctx->prog.bytes;
+    I.gemm_cmac_per_slice = ctx->prog.gemm_cmac;
+    if (info) *info = I;
+    return TN_OK;
+}
+
+tn_status tn_plan_dump(const tn_ctx* ctx, const char* path) {
+    if (!ctx || !path) return TN_EINVAL;
+    if (!ctx->planned) return TN_EINVAL;
+    std::ofstream f(path);
+    if (!f) return TN_EINVAL;
+    f << ctx->prog.dump_json;
+    return TN_OK;
+}
+
+tn_status tn_bind_device(tn_ctx* ctx, int device, void* workspace, size_t bytes, void* cuda_stream) {
+    if (!ctx) return TN_EINVAL;
+    if (!ctx->planned) return fail(ctx, TN_EINVAL, "tn_bind_device before tn_plan");
+    if (ctx->dev) {
+        tnb::dev_destroy(ctx->dev);
+        ctx->dev = nullptr;
+    }
+    std::string e;
+    int rc = tnb::dev_bind(&ctx->dev, ctx->prog, device, workspace, bytes, cuda_stream, ctx->req.M, e);
+    if (rc) return fail(ctx, (tn_status)rc, e);
+    return TN_OK;
+}
+
+tn_status tn_contract(tn_ctx* ctx, const uint64_t* slice_ids, int64_t n_ids, void* amps_out, int32_t out_on_device,
+                      double* seconds_out) {
+    if (!ctx) return TN_EINVAL;
+    if (!ctx->dev) return fail(ctx, TN_EINVAL, "tn_contract before tn_bind_device");
+    if (!slice_ids || n_ids < 1) return fail(ctx, TN_EINVAL, "empty slice subset");
+    if (!amps_out) return fail(ctx, TN_EINVAL, "null amps_out");
+    const int s = (int)ctx->plan.sliced.size();
+    std::vector<uint64_t> ids(slice_ids, slice_ids + n_ids);
+    std::sort(ids.begin(), ids.end());
+    for (int64_t i = 0; i < n_ids; i++) {
+        if (s < 64 && ids[i] >= (1ull << s)) return fail(ctx, TN_EINVAL, "slice id out of range [0, 2^s)");
+        if (i && ids[i] == ids[i - 1]) return fail(ctx, TN_EINVAL, "duplicate slice id");
+    }
+    std::string e;
+    int rc = tnb::dev_contract(ctx->dev, ids.data(), n_ids, amps_out, out_on_device != 0, seconds_out, e);
+    if (rc) return fail(ctx, (tn_status)rc, e);
+    return TN_OK;
+}
+
+tn_status tn_profile_slice(tn_ctx* ctx, uint64_t slice_id, tn_launch_stat* stats, int32_t max_stats,
+                           int32_t* n_stats) {
+    if (!ctx || !stats || !n_stats) return TN_EINVAL;
+    if (!ctx->dev) return fail(ctx, TN_EINVAL, "tn_profile_slice before tn_bind_device");
+    const int s = (int)ctx->plan.sliced.size();
+    if (s < 64 && slice_id >= (1ull << s)) return fail(ctx, TN_EINVAL, "slice id out of range");
+    std::string e;
+    int n = 0;
+    int rc = tnb::dev_profile(ctx->dev, slice_id, stats, max_stats, &n, e);
+    *n_stats = n;
+    if (rc) return fail(ctx, (tn_status)rc, e);
+    return TN_OK;
+}
+
+tn_status tn_sample(const tn_ctx* cctx, const float* amps, const float* ideal_amps, int64_t n_slices_summed,
+                    uint64_t seed, uint64_t* samples_out, double est[3]) {
+    tn_ctx* ctx = const_cast<tn_ctx*>(cctx);
+    if (!ctx || !amps || !samples_out || !est) return TN_EINVAL;
+    const tnb::Request& r = ctx->req;
+    if (r.M < 1) return fail(ctx, TN_EINVAL, "tn_sample before tn_build");
+    const int s = ctx->planned ? (int)ctx->plan.sliced.size() : 0;
+    if (n_slices_summed < 1 || (s < 63 && n_slices_summed > (1ll << s)))
+        return fail(ctx, TN_EINVAL, "n_slices_summed must be in [1, 2^s]");
+    const uint64_t key = rng_key(seed, TAG_SAMPLER);
+    double norm2 = 0.0, xeb_sum = 0.0;
+    for (int64_t g = 0; g < r.L; g++) {
+        const float* a = amps + 2 * g * r.l;
+        // weights |a|^2 = re*re + im*im in fp64, cumulated in ascending mu
+        double tot = 0.0;
+        for (int64_t mu = 0; mu < r.l; mu++) {
+            const double re = (double)a[2 * mu], im = (double)a[2 * mu + 1];
+            const double w = re * re + im * im;
+            tot += w;
+        }
+        if (!(tot > 0.0)) {
+            std::ostringstream o;
+            o << "all-zero group " << g;
+            return fail(ctx, TN_ENUMERIC, o.str());
+        }
+        norm2 += tot;
+        const double u = (double)(rng_word(key, (uint64_t)g) >> 11) * (1.0 / 9007199254740992.0);
+        const double thr = u * tot;
+        double cum = 0.0;
+        int64_t pick = r.l - 1;
+        for (int64_t mu = 0; mu < r.l; mu++) {
+            const double re = (double)a[2 * mu], im = (double)a[2 * mu + 1];
+            const double w = re * re + im * im;
+            cum += w;
+            if (cum > thr) {
+                pick = mu;
+                break;
+            }
+        }
+        const int64_t j = g * r.l + pick;
+        samples_out[g] = r.bits[j];
+        if (ideal_amps) {
+            const double re = ideal_amps[2 * j], im = ideal_amps[2 * j + 1];
+            xeb_sum += re * re + im * im;
+        }
+    }
+    const double N = std::ldexp(1.0, r.n);
+    est[0] = (double)n_slices_summed / std::ldexp(1.0, s);
+    est[1] = N / (double)r.M * norm2;
+    est[2] = ideal_amps ? N / (double)r.L * xeb_sum - 1.0 : std::nan("");
+    return TN_OK;
+}
+
+// ---------------------------------------------------------------------------- debug entries
+
+tn_status tn_debug_gemm_tf32x3(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
+                               void* cuda_stream) {
+    std::string e;
+    int rc = tnb::debug_gemm(A, B, C, M, N, K, cuda_stream, e);
+    return (tn_status)rc;
+}
+
+tn_status tn_debug_network(const tn_ctx* ctx, int64_t* n_tensors, int64_t* n_edges, int64_t* n_internal) {
+    if (!ctx || ctx->leaves.empty()) return TN_EINVAL;
+    int64_t alive = 0, internal = 0;
+    for (auto& t : ctx->net.tensors) alive += t.alive;
+    for (auto& E : ctx->net.edges)
+        if (!E.output && E.t1 >= 0 && ctx->net.tensors[E.t0].alive && ctx->net.tensors[E.t1].alive) internal++;
+    if (n_tensors) *n_tensors = alive;
+    if (n_edges) *n_edges = (int64_t)ctx->net.edges.size();
+    if (n_internal) *n_internal = internal;
+    return TN_OK;
+}
+
+}  // extern "C"

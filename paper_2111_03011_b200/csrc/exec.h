@@ -1,0 +1,21 @@
+// exec.h -- host interface of the device executor (executor.cu).
+#pragma once
+
+#include <string>
+
+#include "tnb.h"
+
+namespace tnb {
+
+struct Device;
+
+int dev_bind(Device** out, const Program& prog, int device, void* workspace, size_t bytes, void* stream, int64_t M,
+             std::string& err);
+int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_out, bool out_dev, double* secs,
+                 std::string& err);
+int dev_profile(Device* d, uint64_t slice_id, tn_launch_stat* stats, int max_stats, int* n_stats, std::string& err);
+void dev_destroy(Device* d);
+int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K, void* stream,
+               std::string& err);
+
+}  // namespace tnb

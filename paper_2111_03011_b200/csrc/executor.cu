@@ -1,0 +1,634 @@
+// executor.cu -- device runtime of the slice program: upload (leaf bank, row maps, index tables),
+// per-slice CUDA graph, the tn_contract loop, and per-launch profiling.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "exec.h"
+#include "gemm_tc.cuh"
+#include "kernels.cuh"
+#include "tnb.h"
+
+namespace tnb {
+
+namespace {
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess) {                                                           \
+            err = std::string(#x) + " failed: " + cudaGetErrorString(e_);                  \
+            return TN_ECUDA;                                                               \
+        }                                                                                  \
+    } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+// 2D fp32 tensor map [rows][cols] row-major, box 128 rows x 32 cols, 128B swizzle
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(cols * 4)};
+    cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)tc::BM};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// byte-sliced offset tables: for index bits [8t, 8t+8) -> sum of 1 << dst-positions
+void push_tables(std::vector<uint32_t>& out, const std::vector<int>& src_of_bit, int ncols, int col) {
+    // src_of_bit[b] = target bit of index bit b (-1 = none); writes ntab*256 entries of stride ncols
+    int nb = (int)src_of_bit.size();
+    int nt = (nb + 7) / 8;
+    for (int t = 0; t < nt; t++)
+        for (int v = 0; v < 256; v++) {
+            uint32_t s = 0;
+            for (int b = 0; b < 8; b++) {
+                int bit = 8 * t + b;
+                if (bit < nb && ((v >> b) & 1) && src_of_bit[bit] >= 0) s += 1u << src_of_bit[bit];
+            }
+            out[((size_t)t * 256 + v) * ncols + col] = s;
+        }
+}
+
+struct Launch {
+    int kind = 0;
+    int pair = -1;
+    double cmac = 0, bytes = 0;
+    int64_t m = 0, n = 0, k = 0, rows = 0;
+    dim3 grid, block;
+    size_t smem = 0;
+    // per-kind parameters
+    kern::ApplyDev ap;
+    int ni = 0, team = 1;
+    kern::PrepADev pa;
+    kern::PrepBDev pb;
+    CUtensorMap tm[4];
+    float* gC = nullptr;
+    int64_t gMp = 0, gN2 = 0, gK2 = 0;
+    // instantiate / readout
+    const InstLeafDesc* itab = nullptr;
+    int in_leaves = 0;
+    int64_t in_items = 0;
+    const float2* F = nullptr;
+    const int64_t* ridx = nullptr;
+    int64_t M = 0;
+};
+
+}  // namespace
+
+struct Device {
+    int dev = 0;
+    cudaStream_t user = nullptr, stream = nullptr;
+    char* bank = nullptr;
+    char* maps = nullptr;
+    char* work = nullptr;
+    bool own_work = false;
+    uint32_t* tables = nullptr;
+    double2* acc = nullptr;
+    float2* out = nullptr;
+    uint64_t* slice_ids = nullptr;
+    int64_t slice_cap = 0;
+    int64_t* counter = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evu = nullptr;
+    std::vector<Launch> launches;
+    int64_t M = 0;
+    int s = 0;
+};
+
+namespace {
+
+template <int NI, int TEAM>
+void launch_apply(const Launch& L, cudaStream_t st) {
+    kern::k_apply<NI, TEAM><<<L.grid, L.block, L.smem, st>>>(L.ap);
+}
+
+template <int TEAM>
+void launch_apply_ni(const Launch& L, cudaStream_t st) {
+    switch (L.ni) {
+        case 0: launch_apply<0, TEAM>(L, st); break;
+        case 1: launch_apply<1, TEAM>(L, st); break;
+        case 2: launch_apply<2, TEAM>(L, st); break;
+        case 3: launch_apply<3, TEAM>(L, st); break;
+        default: launch_apply<4, TEAM>(L, st); break;
+    }
+}
+
+int set_smem_attrs(std::string& err) {
+    static bool done = false;
+    if (done) return TN_OK;
+    const int big = 160 * 1024;
+#define SETA(NI, T) CK(cudaFuncSetAttribute(kern::k_apply<NI, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, big))
+    SETA(0, 1); SETA(1, 1); SETA(2, 1); SETA(3, 1); SETA(4, 1);
+    SETA(0, 32); SETA(1, 32); SETA(2, 32); SETA(3, 32); SETA(4, 32);
+#undef SETA
+    CK(cudaFuncSetAttribute(kern::k_prep_a, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    CK(cudaFuncSetAttribute(kern::k_prep_b, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES));
+    done = true;
+    return TN_OK;
+}
+
+void do_launch(Device* d, const Launch& L, cudaStream_t st) {
+    switch (L.kind) {
+        case K_INSTANTIATE:
+            kern::k_instantiate<<<L.grid, L.block, 0, st>>>(L.itab, L.in_leaves, L.in_items, (const float2*)d->bank,
+                                                            d->work, d->slice_ids, d->counter, d->s);
+            break;
+        case K_APPLY:
+            if (L.team == 32) launch_apply_ni<32>(L, st);
+            else launch_apply_ni<1>(L, st);
+            break;
+        case K_PREP_A:
+            kern::k_prep_a<<<L.grid, L.block, L.smem, st>>>(L.pa);
+            break;
+        case K_PREP_B:
+            kern::k_prep_b<<<L.grid, L.block, L.smem, st>>>(L.pb);
+            break;
+        case K_GEMM:
+            tc::k_gemm_tf32x3<<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp, L.gN2, L.gK2);
+            break;
+        case K_READOUT:
+            kern::k_readout<<<L.grid, L.block, 0, st>>>(L.F, L.ridx, d->acc, L.M, d->counter);
+            break;
+    }
+}
+
+dim3 grid_for(int64_t threads, int64_t per_block = 256, int64_t cap = 148 * 16) {
+    int64_t b = (threads + per_block - 1) / per_block;
+    b = std::max<int64_t>(1, std::min(b, cap));
+    return dim3((unsigned)b);
+}
+
+}  // namespace
+
+int dev_bind(Device** out, const Program& prog, int device, void* workspace, size_t bytes, void* stream, int64_t M,
+             std::string& err) {
+    *out = nullptr;
+    Device* d = new Device();
+    auto fail = [&](int code) {
+        dev_destroy(d);
+        return code;
+    };
+    d->dev = device;
+    d->M = M;
+    d->s = prog.s;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        err = "cudaSetDevice failed (no GPU?)";
+        delete d;
+        return TN_ECUDA;
+    }
+    {
+        int rc = set_smem_attrs(err);
+        if (rc) return fail(rc);
+    }
+    d->user = (cudaStream_t)stream;
+#define CKF(x)                                                                   \
+    do {                                                                         \
+        cudaError_t e_ = (x);                                                    \
+        if (e_ != cudaSuccess) {                                                 \
+            err = std::string(#x) + " failed: " + cudaGetErrorString(e_);        \
+            return fail(TN_ECUDA);                                               \
+        }                                                                        \
+    } while (0)
+    CKF(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+    CKF(cudaEventCreate(&d->ev0));
+    CKF(cudaEventCreate(&d->ev1));
+    CKF(cudaEventCreateWithFlags(&d->evu, cudaEventDisableTiming));
+    if (workspace) {
+        if ((int64_t)bytes < prog.work_bytes) {
+            std::ostringstream o;
+            o << "workspace too small: need " << prog.work_bytes << " bytes, got " << bytes;
+            err = o.str();
+            return fail(TN_ENOMEM);
+        }
+        d->work = (char*)workspace;
+    } else {
+        if (cudaMalloc(&d->work, prog.work_bytes) != cudaSuccess) {
+            err = "cudaMalloc(workspace) failed";
+            return fail(TN_ENOMEM);
+        }
+        d->own_work = true;
+    }
+    CKF(cudaMalloc(&d->bank, std::max<size_t>(prog.bank.size() * 4, 16)));
+    CKF(cudaMemcpy(d->bank, prog.bank.data(), prog.bank.size() * 4, cudaMemcpyHostToDevice));
+    CKF(cudaMalloc(&d->maps, std::max<size_t>(prog.maps.size(), 16)));
+    if (!prog.maps.empty()) CKF(cudaMemcpy(d->maps, prog.maps.data(), prog.maps.size(), cudaMemcpyHostToDevice));
+    CKF(cudaMalloc(&d->acc, std::max<int64_t>(M, 1) * sizeof(double2)));
+    CKF(cudaMalloc(&d->out, std::max<int64_t>(M, 1) * sizeof(float2)));
+    CKF(cudaMalloc(&d->counter, sizeof(int64_t)));
+    d->slice_cap = 1024;
+    CKF(cudaMalloc(&d->slice_ids, d->slice_cap * sizeof(uint64_t)));
+    CKF(cudaMemset(d->slice_ids, 0, d->slice_cap * sizeof(uint64_t)));
+    CKF(cudaMemset(d->counter, 0, sizeof(int64_t)));
+
+    auto ptr = [&](const BufRef& b) -> char* {
+        switch (b.region) {
+            case REG_WORK: return d->work + b.offset;
+            case REG_BANK: return d->bank + b.offset;
+            case REG_MAPS: return d->maps + b.offset;
+            default: return nullptr;
+        }
+    };
+
+    // ---------------------------------------------------------------- index tables (host build)
+    std::vector<uint32_t> tabs;  // concatenated; offsets recorded per launch (in uint32 units)
+    struct TabFix { size_t launch; int which; size_t off; };
+    std::vector<TabFix> fixes;
+    for (const Step& st : prog.steps) {
+        Launch L;
+        L.kind = st.kind;
+        L.pair = st.pair;
+        L.cmac = st.cmac;
+        L.bytes = st.bytes;
+        L.block = dim3(256);
+        if (st.kind == K_INSTANTIATE) {
+            L.itab = (const InstLeafDesc*)ptr(st.ip.table);
+            L.in_leaves = st.ip.n_leaves;
+            L.in_items = st.ip.n_items;
+            L.grid = grid_for(st.ip.n_items);
+        } else if (st.kind == K_APPLY) {
+            const ApplyParams& a = st.ap;
+            kern::ApplyDev& p = L.ap;
+            std::memset(&p, 0, sizeof(p));
+            p.A = (const float2*)ptr(a.A);
+            p.B = (const float2*)ptr(a.B);
+            p.C = (float2*)ptr(a.C);
+            p.ma = (const int32_t*)ptr(a.ma);
+            p.mb = (const int32_t*)ptr(a.mb);
+            p.R = a.R;
+            p.a_row = a.a_row;
+            p.b_row = a.b_row;
+            p.c_row = a.c_row;
+            p.nk = a.nk;
+            for (int t = 0; t < a.nk; t++) {
+                p.kA[t] = a.kA[t];
+                p.kB[t] = a.kB[t];
+            }
+            // classify C bits
+            std::vector<int> a_of_c(a.dC, -1), b_of_c(a.dC, -1);
+            for (int i = 0; i < a.cA.n; i++) a_of_c[a.cA.dst[i]] = a.cA.src[i];
+            for (int i = 0; i < a.cB.n; i++) b_of_c[a.cB.dst[i]] = a.cB.src[i];
+            std::vector<bool> inner(a.dC, false);
+            for (int u = 0; u < a.n_inner; u++) inner[a.inner_c[u]] = true;
+            std::vector<int> orb;  // orbit bit t -> C bit
+            for (int c = 0; c < a.dC; c++)
+                if (!inner[c]) orb.push_back(c);
+            const int nob = (int)orb.size();
+            p.n_orbits = (int64_t)1 << nob;
+            p.ntab = (nob + 7) / 8;
+            for (int ii = 0; ii < (1 << a.n_inner); ii++) {
+                uint32_t co = 0, bo = 0;
+                for (int u = 0; u < a.n_inner; u++)
+                    if ((ii >> u) & 1) {
+                        co += 1u << a.inner_c[u];
+                        bo += 1u << b_of_c[a.inner_c[u]];
+                    }
+                p.inner_c[ii] = co;
+                p.inner_b[ii] = bo;
+            }
+            L.ni = a.n_inner;
+            size_t base = tabs.size();
+            tabs.resize(base + (size_t)std::max(p.ntab, 0) * 256 * 4, 0);
+            {
+                std::vector<int> cc(nob), aa(nob), bb(nob);
+                for (int t = 0; t < nob; t++) {
+                    cc[t] = orb[t];
+                    aa[t] = a_of_c[orb[t]];
+                    bb[t] = b_of_c[orb[t]];
+                }
+                std::vector<uint32_t> tmp((size_t)p.ntab * 256 * 4, 0);
+                push_tables(tmp, cc, 4, 0);
+                push_tables(tmp, aa, 4, 1);
+                push_tables(tmp, bb, 4, 2);
+                std::copy(tmp.begin(), tmp.end(), tabs.begin() + base);
+            }
+            fixes.push_back({d->launches.size(), 0, base});
+            size_t kbase = 0;
+            if (a.nk <= kern::KTAB_MAX_BITS) {
+                kbase = tabs.size();
+                tabs.resize(kbase + ((size_t)2 << a.nk), 0);
+                for (int64_t kk = 0; kk < ((int64_t)1 << a.nk); kk++) {
+                    uint32_t ka = 0, kb = 0;
+                    for (int t = 0; t < a.nk; t++)
+                        if ((kk >> t) & 1) {
+                            ka += 1u << a.kA[t];
+                            kb += 1u << a.kB[t];
+                        }
+                    tabs[kbase + 2 * kk] = ka;
+                    tabs[kbase + 2 * kk + 1] = kb;
+                }
+                fixes.push_back({d->launches.size(), 1, kbase});
+            }
+            const int64_t total = a.R * p.n_orbits;
+            L.team = (total < 148 * 512 && a.nk >= 4) ? 32 : 1;
+            L.grid = grid_for(total * L.team, 256, 148 * 8);
+            L.smem = (size_t)p.ntab * 256 * 4 * 4 + (a.nk <= kern::KTAB_MAX_BITS ? ((size_t)8 << a.nk) : 0);
+            L.m = p.n_orbits;
+            L.n = (int64_t)1 << a.n_inner;
+            L.k = (int64_t)1 << a.nk;
+            L.rows = a.R;
+        } else if (st.kind == K_PREP_A || st.kind == K_PREP_B || st.kind == K_GEMM) {
+            const GemmParams& g = st.gp;
+            const int lm = (int)g.aM.n, lk = (int)g.aK.n, ln = (int)g.bN.n;
+            const int64_t Mp = g.R * g.m;
+            L.m = Mp;
+            L.n = g.n;
+            L.k = g.k;
+            L.rows = g.R;
+            if (st.kind == K_PREP_A) {
+                kern::PrepADev& p = L.pa;
+                p.A = (const float2*)ptr(g.A);
+                p.ma = (const int32_t*)ptr(g.ma);
+                p.hi = (float2*)ptr(g.Ahi);
+                p.lo = (float2*)ptr(g.Alo);
+                p.Mp = Mp;
+                p.K = g.k;
+                p.a_row = g.a_row;
+                p.log2m = lm;
+                p.log2k = lk;
+                p.ntm = (lm + 7) / 8;
+                p.ntk = (lk + 7) / 8;
+                std::vector<int> mm(lm), kk(lk);
+                for (int t = 0; t < lm; t++) mm[g.aM.dst[t]] = g.aM.src[t];
+                for (int t = 0; t < lk; t++) kk[g.aK.dst[t]] = g.aK.src[t];
+                size_t base = tabs.size();
+                std::vector<uint32_t> t1((size_t)p.ntm * 256, 0), t2((size_t)p.ntk * 256, 0);
+                if (p.ntm) push_tables(t1, mm, 1, 0);
+                if (p.ntk) push_tables(t2, kk, 1, 0);
+                tabs.insert(tabs.end(), t1.begin(), t1.end());
+                tabs.insert(tabs.end(), t2.begin(), t2.end());
+                fixes.push_back({d->launches.size(), 2, base});
+                L.smem = (size_t)(p.ntm + p.ntk) * 256 * 4;
+                L.grid = grid_for(Mp * g.k, 256, 148 * 16);
+            } else if (st.kind == K_PREP_B) {
+                kern::PrepBDev& p = L.pb;
+                p.B = (const float2*)ptr(g.B);
+                p.hi = (float2*)ptr(g.Bhi);
+                p.lo = (float2*)ptr(g.Blo);
+                p.N = g.n;
+                p.K = g.k;
+                p.log2k = lk;
+                p.ntn = (ln + 7) / 8;
+                p.ntk = (lk + 7) / 8;
+                std::vector<int> nn(ln), kk(lk);
+                for (int t = 0; t < ln; t++) nn[g.bN.dst[t]] = g.bN.src[t];
+                for (int t = 0; t < lk; t++) kk[g.bK.dst[t]] = g.bK.src[t];
+                size_t base = tabs.size();
+                std::vector<uint32_t> t1((size_t)p.ntn * 256, 0), t2((size_t)p.ntk * 256, 0);
+                if (p.ntn) push_tables(t1, nn, 1, 0);
+                if (p.ntk) push_tables(t2, kk, 1, 0);
+                tabs.insert(tabs.end(), t1.begin(), t1.end());
+                tabs.insert(tabs.end(), t2.begin(), t2.end());
+                fixes.push_back({d->launches.size(), 3, base});
+                L.smem = (size_t)(p.ntn + p.ntk) * 256 * 4;
+                L.grid = grid_for(g.n * g.k, 256, 148 * 16);
+            } else {
+                const int64_t N2 = 2 * g.n, K2 = 2 * g.k;
+                if (!make_map(&L.tm[0], ptr(g.Ahi), Mp, K2) || !make_map(&L.tm[1], ptr(g.Alo), Mp, K2) ||
+                    !make_map(&L.tm[2], ptr(g.Bhi), N2, K2) || !make_map(&L.tm[3], ptr(g.Blo), N2, K2)) {
+                    err = "cuTensorMapEncodeTiled failed";
+                    return fail(TN_ECUDA);
+                }
+                L.gC = (float*)ptr(g.C);
+                L.gMp = Mp;
+                L.gN2 = N2;
+                L.gK2 = K2;
+                L.grid = dim3((unsigned)((Mp + tc::BM - 1) / tc::BM), (unsigned)(N2 / tc::BN));
+                L.block = dim3(tc::THREADS);
+                L.smem = tc::SMEM_BYTES;
+            }
+        } else if (st.kind == K_READOUT) {
+            L.F = (const float2*)ptr(st.rp.F);
+            L.ridx = (const int64_t*)ptr(st.rp.idx);
+            L.M = st.rp.M;
+            L.grid = grid_for(st.rp.M, 256, 148 * 8);
+        }
+        d->launches.push_back(L);
+    }
+    if (!tabs.empty()) {
+        CKF(cudaMalloc(&d->tables, tabs.size() * 4));
+        CKF(cudaMemcpy(d->tables, tabs.data(), tabs.size() * 4, cudaMemcpyHostToDevice));
+    }
+    for (const TabFix& f : fixes) {
+        Launch& L = d->launches[f.launch];
+        const uint32_t* p = d->tables + f.off;
+        if (f.which == 0) L.ap.tab = p;
+        else if (f.which == 1) L.ap.ktab = p;
+        else if (f.which == 2) L.pa.tab = p;
+        else L.pb.tab = p;
+    }
+
+    // ---------------------------------------------------------------- capture the per-slice graph
+    CKF(cudaStreamBeginCapture(d->stream, cudaStreamCaptureModeThreadLocal));
+    for (const Launch& L : d->launches) do_launch(d, L, d->stream);
+    cudaError_t ce = cudaStreamEndCapture(d->stream, &d->graph);
+    if (ce != cudaSuccess) {
+        err = std::string("graph capture failed: ") + cudaGetErrorString(ce);
+        return fail(TN_ECUDA);
+    }
+    CKF(cudaGraphInstantiate(&d->gexec, d->graph, 0));
+    CKF(cudaStreamSynchronize(d->stream));
+#undef CKF
+    *out = d;
+    return TN_OK;
+}
+
+int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_out, bool out_dev, double* secs,
+                 std::string& err) {
+    CK(cudaSetDevice(d->dev));
+    if (n > d->slice_cap) {
+        CK(cudaFree(d->slice_ids));
+        d->slice_cap = std::max<int64_t>(n, 2 * d->slice_cap);
+        CK(cudaMalloc(&d->slice_ids, d->slice_cap * sizeof(uint64_t)));
+    }
+    // order after the caller's pending work
+    CK(cudaEventRecord(d->evu, d->user));
+    CK(cudaStreamWaitEvent(d->stream, d->evu, 0));
+    CK(cudaMemcpyAsync(d->slice_ids, ids_sorted, n * sizeof(uint64_t), cudaMemcpyHostToDevice, d->stream));
+    CK(cudaMemsetAsync(d->acc, 0, d->M * sizeof(double2), d->stream));
+    CK(cudaMemsetAsync(d->counter, 0, sizeof(int64_t), d->stream));
+    CK(cudaEventRecord(d->ev0, d->stream));
+    for (int64_t i = 0; i < n; i++) CK(cudaGraphLaunch(d->gexec, d->stream));
+    float2* dst = out_dev ? (float2*)amps_out : d->out;
+    kern::k_finalize<<<grid_for(d->M, 256, 148 * 8), 256, 0, d->stream>>>(d->acc, dst, d->M);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(d->ev1, d->stream));
+    if (!out_dev) {
+        CK(cudaMemcpyAsync(amps_out, d->out, d->M * sizeof(float2), cudaMemcpyDeviceToHost, d->stream));
+        CK(cudaStreamSynchronize(d->stream));
+    } else {
+        CK(cudaEventRecord(d->evu, d->stream));
+        CK(cudaStreamWaitEvent(d->user, d->evu, 0));
+    }
+    if (secs) {
+        CK(cudaEventSynchronize(d->ev1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, d->ev0, d->ev1));
+        *secs = ms * 1e-3;
+    }
+    return TN_OK;
+}
+
+int dev_profile(Device* d, uint64_t slice_id, tn_launch_stat* stats, int max_stats, int* n_stats, std::string& err) {
+    CK(cudaSetDevice(d->dev));
+    CK(cudaStreamSynchronize(d->user));
+    CK(cudaMemcpyAsync(d->slice_ids, &slice_id, sizeof(uint64_t), cudaMemcpyHostToDevice, d->stream));
+    CK(cudaMemsetAsync(d->counter, 0, sizeof(int64_t), d->stream));
+    CK(cudaMemsetAsync(d->acc, 0, d->M * sizeof(double2), d->stream));
+    const int nl = (int)d->launches.size();
+    std::vector<cudaEvent_t> ev(nl + 1);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(ev[0], d->stream));
+    for (int i = 0; i < nl; i++) {
+        do_launch(d, d->launches[i], d->stream);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ev[i + 1], d->stream));
+    }
+    CK(cudaStreamSynchronize(d->stream));
+    int w = 0;
+    for (int i = 0; i < nl && w < max_stats; i++, w++) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+        const Launch& L = d->launches[i];
+        tn_launch_stat& s = stats[w];
+        s.kind = L.kind;
+        s.step = L.pair;
+        s.cmac = L.cmac;
+        s.bytes = L.bytes;
+        s.ms = ms;
+        s.m = L.m;
+        s.n = L.n;
+        s.k = L.k;
+        s.rows = L.rows;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    *n_stats = w;
+    return TN_OK;
+}
+
+void dev_destroy(Device* d) {
+    if (!d) return;
+    cudaSetDevice(d->dev);
+    if (d->stream) cudaStreamSynchronize(d->stream);
+    if (d->gexec) cudaGraphExecDestroy(d->gexec);
+    if (d->graph) cudaGraphDestroy(d->graph);
+    if (d->own_work && d->work) cudaFree(d->work);
+    cudaFree(d->bank);
+    cudaFree(d->maps);
+    cudaFree(d->tables);
+    cudaFree(d->acc);
+    cudaFree(d->out);
+    cudaFree(d->slice_ids);
+    cudaFree(d->counter);
+    if (d->ev0) cudaEventDestroy(d->ev0);
+    if (d->ev1) cudaEventDestroy(d->ev1);
+    if (d->evu) cudaEventDestroy(d->evu);
+    if (d->stream) cudaStreamDestroy(d->stream);
+    delete d;
+}
+
+// ---------------------------------------------------------------------------- debug / unit entry
+// C[M][N] = A[M][K] B[K][N], complex64 row-major device buffers, through the tensor-core path
+// (prep A / prep B / tcgen05 GEMM).  M % 128 may be ragged; N >= 64 and K >= 16 powers of two.
+int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K, void* stream,
+               std::string& err) {
+    if (set_smem_attrs(err)) return TN_ECUDA;
+    if (N < 64 || K < 16 || (N & (N - 1)) || (K & (K - 1))) {
+        err = "debug_gemm: N >= 64 and K >= 16 must be powers of two";
+        return TN_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    float *ahi, *alo, *bhi, *blo;
+    CK(cudaMalloc(&ahi, M * K * 8));
+    CK(cudaMalloc(&alo, M * K * 8));
+    CK(cudaMalloc(&bhi, N * K * 16));
+    CK(cudaMalloc(&blo, N * K * 16));
+    int lk = 0, ln = 0;
+    while ((1ll << lk) < K) lk++;
+    while ((1ll << ln) < N) ln++;
+    // A: m index bits -> A bits (row-major [M][K]: m bit b -> bit b + lk), k bits -> bits 0..lk-1.
+    // Use R = M rows of m = 1 so that ragged M works: A row stride = K.
+    std::vector<uint32_t> tab;
+    std::vector<int> kk(lk), nn(ln), kb(lk);
+    for (int t = 0; t < lk; t++) kk[t] = t;
+    std::vector<uint32_t> tk((size_t)((lk + 7) / 8) * 256, 0);
+    push_tables(tk, kk, 1, 0);
+    // B[k][n]: k bit t -> bit t + ln, n bit t -> bit t
+    for (int t = 0; t < ln; t++) nn[t] = t;
+    for (int t = 0; t < lk; t++) kb[t] = t + ln;
+    std::vector<uint32_t> tn((size_t)((ln + 7) / 8) * 256, 0), tkb((size_t)((lk + 7) / 8) * 256, 0);
+    push_tables(tn, nn, 1, 0);
+    push_tables(tkb, kb, 1, 0);
+    tab.insert(tab.end(), tk.begin(), tk.end());
+    size_t off_b = tab.size();
+    tab.insert(tab.end(), tn.begin(), tn.end());
+    tab.insert(tab.end(), tkb.begin(), tkb.end());
+    uint32_t* dtab;
+    CK(cudaMalloc(&dtab, tab.size() * 4));
+    CK(cudaMemcpy(dtab, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+    kern::PrepADev pa;
+    pa.A = (const float2*)A;
+    pa.ma = nullptr;
+    pa.hi = (float2*)ahi;
+    pa.lo = (float2*)alo;
+    pa.Mp = M;
+    pa.K = K;
+    pa.a_row = K;
+    pa.log2m = 0;
+    pa.log2k = lk;
+    pa.tab = dtab;
+    pa.ntm = 0;
+    pa.ntk = (lk + 7) / 8;
+    kern::k_prep_a<<<grid_for(M * K), 256, (size_t)pa.ntk * 1024, st>>>(pa);
+    kern::PrepBDev pb;
+    pb.B = (const float2*)B;
+    pb.hi = (float2*)bhi;
+    pb.lo = (float2*)blo;
+    pb.N = N;
+    pb.K = K;
+    pb.log2k = lk;
+    pb.tab = dtab + off_b;
+    pb.ntn = (ln + 7) / 8;
+    pb.ntk = (lk + 7) / 8;
+    kern::k_prep_b<<<grid_for(N * K), 256, (size_t)(pb.ntn + pb.ntk) * 1024, st>>>(pb);
+    CUtensorMap tm[4];
+    if (!make_map(&tm[0], ahi, M, 2 * K) || !make_map(&tm[1], alo, M, 2 * K) || !make_map(&tm[2], bhi, 2 * N, 2 * K) ||
+        !make_map(&tm[3], blo, 2 * N, 2 * K)) {
+        err = "cuTensorMapEncodeTiled failed";
+        return TN_ECUDA;
+    }
+    dim3 grid((unsigned)((M + tc::BM - 1) / tc::BM), (unsigned)(2 * N / tc::BN));
+    tc::k_gemm_tf32x3<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(tm[0], tm[1], tm[2], tm[3], C, M, 2 * N, 2 * K);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    cudaFree(ahi);
+    cudaFree(alo);
+    cudaFree(bhi);
+    cudaFree(blo);
+    cudaFree(dtab);
+    return TN_OK;
+}
+
+}  // namespace tnb

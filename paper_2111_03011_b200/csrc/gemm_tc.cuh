@@ -1,0 +1,210 @@
+// gemm_tc.cuh -- complex64 pairwise contraction on the 5th-gen tensor cores.
+//
+// The complex GEMM C = A B (complex64, C[m][n] = sum_k A[m][k] B[k][n]) is run as one real GEMM via
+// the complex-as-real embedding:
+//   A_real [Mp][2K] = A interleaved (re, im) along K         (K-major as stored)
+//   Bt     [2N][2K] : row 2n = (br, -bi) pairs, row 2n+1 = (bi, br) pairs along K   (K-major)
+//   C_real [Mp][2N] = A_real Bt^T  = complex C interleaved.
+// 3xTF32 keeps fp32-level accuracy on the TF32 tensor cores:
+//   x = hi + lo, hi = cvt.rna.tf32(x), lo = x - hi;  C = Ahi Bhi + Ahi Blo + Alo Bhi  (lo*lo dropped),
+// all three products accumulated in one fp32 TMEM accumulator.
+//
+// Kernel anatomy (sm_100a): one 128x128 output tile per CTA, 128 threads.
+//   warp 0 / lane 0 : TMA producer (cp.async.bulk.tensor, SWIZZLE_128B) into a 3-stage smem ring,
+//                     four 128x32 fp32 tiles per stage (Ahi, Alo, Bhi, Blo), mbarrier full/empty.
+//   warp 1 / lane 0 : MMA issuer, tcgen05.mma.cta_group::1.kind::tf32 M=128 N=128 K=8, 12 per stage,
+//                     tcgen05.commit -> empty barrier; last stage commits to the accumulator barrier.
+//   warp 2          : TMEM allocation (128 columns) / deallocation.
+//   warps 0-3       : epilogue, tcgen05.ld 32x32b (lane quarter = warp id) -> registers -> global.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tnb {
+namespace tc {
+
+constexpr int BM = 128;          // rows of A per tile (MMA M)
+constexpr int BN = 128;          // rows of Bt per tile (MMA N, real columns of C)
+constexpr int BK = 32;           // fp32 elements per k-block = 128 B = one swizzle atom row
+constexpr int STAGES = 3;
+constexpr int TILE_BYTES = BM * BK * 4;              // 16 KB (BM == BN)
+constexpr int STAGE_BYTES = 4 * TILE_BYTES;          // Ahi, Alo, Bhi, Blo
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int THREADS = 128;
+constexpr int TMEM_COLS = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_128B: start>>4, LBO = 1 (16 B, unused for
+// swizzled K-major), SBO = 1024 B (8 rows x 128 B), version 1 (sm_100), layout type 2 (SW128).
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+// instruction descriptor: D fp32 (bit 4), A/B tf32 (format 2 at bits 7, 10), K-major both,
+// N >> 3 at bit 17, M >> 4 at bit 24.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gemm_tf32x3(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
+                  const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
+                  float* __restrict__ C, int64_t Mp, int64_t N2, int64_t K2) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* accb = empty + STAGES;
+    uint32_t* tmem_slot = (uint32_t*)(accb + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * BM;
+    const int n0 = blockIdx.y * BN;
+    const int nkb = (int)(K2 / BK);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accb, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ------------------------------------------------------------ TMA producer
+        for (int kb = 0; kb < nkb; kb++) {
+            const int s = kb % STAGES;
+            const uint32_t ph = (kb / STAGES) & 1;
+            if (kb >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+            uint8_t* st = smem + s * STAGE_BYTES;
+            mbar_expect_tx(&full[s], STAGE_BYTES);
+            const int kc = kb * BK;
+            tma_load_2d(st + 0 * TILE_BYTES, &mAhi, &full[s], kc, m0);
+            tma_load_2d(st + 1 * TILE_BYTES, &mAlo, &full[s], kc, m0);
+            tma_load_2d(st + 2 * TILE_BYTES, &mBhi, &full[s], kc, n0);
+            tma_load_2d(st + 3 * TILE_BYTES, &mBlo, &full[s], kc, n0);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ------------------------------------------------------------ MMA issuer
+        const uint32_t idesc = idesc_tf32(BM, BN);
+        for (int kb = 0; kb < nkb; kb++) {
+            const int s = kb % STAGES;
+            const uint32_t ph = (kb / STAGES) & 1;
+            mbar_wait(&full[s], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / 8; k++) {
+                const uint32_t koff = k * 32;  // 8 tf32 = 32 B along the swizzled 128 B row
+                const uint64_t dAhi = sdesc_sw128(st + 0 * TILE_BYTES + koff);
+                const uint64_t dAlo = sdesc_sw128(st + 1 * TILE_BYTES + koff);
+                const uint64_t dBhi = sdesc_sw128(st + 2 * TILE_BYTES + koff);
+                const uint64_t dBlo = sdesc_sw128(st + 3 * TILE_BYTES + koff);
+                const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
+                mma_tf32(tmem, dAlo, dBhi, idesc, first);  // small terms first
+                mma_tf32(tmem, dAhi, dBlo, idesc, 1u);
+                mma_tf32(tmem, dAhi, dBhi, idesc, 1u);
+            }
+            mma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+        }
+        mma_commit(accb);
+    }
+    __syncwarp();
+
+    // ---------------------------------------------------------------- epilogue (all 4 warps)
+    mbar_wait(accb, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int row = warp * 32 + lane;  // TMEM lane = tile row
+    const int64_t gm = (int64_t)m0 + row;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (gm < Mp) {
+            float4* dst = (float4*)(C + gm * N2 + n0 + c0);
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+                dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                     __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 2) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
+}  // namespace tc
+}  // namespace tnb

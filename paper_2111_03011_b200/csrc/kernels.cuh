@@ -1,0 +1,233 @@
+// kernels.cuh -- the bandwidth-bound kernels of one slice.
+//
+// Index arithmetic: every tensor is [rows][2^d] complex64 with its legs as the bits of the dense
+// index.  Bit permutations are evaluated with byte-sliced lookup tables staged in shared memory:
+// offset(x) = sum_t tab[t][(x >> 8t) & 255], i.e. a pdep/pext of up to 40 bits in <= 5 LDS + adds.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tnb.h"
+
+namespace tnb {
+namespace kern {
+
+__device__ __forceinline__ float2 cmac(float2 acc, float2 a, float2 b) {
+    acc.x = fmaf(a.x, b.x, acc.x);
+    acc.x = fmaf(-a.y, b.y, acc.x);
+    acc.y = fmaf(a.x, b.y, acc.y);
+    acc.y = fmaf(a.y, b.x, acc.y);
+    return acc;
+}
+
+// ---------------------------------------------------------------------------- K1: slice instantiate
+// (row a2) sigma -> v_j = (sigma >> (s-1-j)) & 1; copies the v-part of every sliced leaf from the bank.
+__global__ void k_instantiate(const InstLeafDesc* __restrict__ tab, int n_leaves, int64_t n_items,
+                              const float2* __restrict__ bank, char* __restrict__ work,
+                              const uint64_t* __restrict__ slice_ids, const int64_t* __restrict__ counter, int s) {
+    const uint64_t sigma = slice_ids[*counter];
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < n_items;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        int l = 0;
+        while (l + 1 < n_leaves && tab[l + 1].item_begin <= it) l++;
+        const InstLeafDesc& d = tab[l];
+        const int64_t local = it - d.item_begin;
+        const int64_t r = local >> d.d_out;
+        const int64_t o = local & (((int64_t)1 << d.d_out) - 1);
+        int64_t src = 0;
+        for (int b = 0; b < d.d_out; b++)
+            if ((o >> b) & 1) src |= (int64_t)1 << d.out_src[b];
+        for (int j = 0; j < d.n_sl; j++)
+            if ((sigma >> (s - 1 - d.sl_idx[j])) & 1) src |= (int64_t)1 << d.sl_pos[j];
+        float2* out = (float2*)(work + d.out_off);
+        out[local] = bank[d.bank_off + (r << d.d_full) + src];
+    }
+}
+
+// ---------------------------------------------------------------------------- K3b/K4: sparse-row apply
+// (rows a5, a6) C[r][c] = sum_kk A[ma[r]][offA(c,kk)] * B[mb[r]][offB(c,kk)].
+// A "team" of TEAM threads owns one orbit (a C index with its NI inner bits free): each member sums a
+// strided share of kk for the 2^NI outputs, then the team reduces with warp shuffles (deterministic).
+struct ApplyDev {
+    const float2* A;
+    const float2* B;
+    float2* C;
+    const int32_t* ma;
+    const int32_t* mb;
+    int64_t R, a_row, b_row, c_row, n_orbits;
+    const uint32_t* tab;   // [ntab][256][4] = (c_off, a_off, b_off, 0) of the orbit index bytes
+    const uint32_t* ktab;  // [2^nk][2] = (a_off, b_off) of kk, when nk <= KTAB_MAX_BITS
+    int ntab, nk;
+    int8_t kA[40], kB[40];
+    uint32_t inner_c[16], inner_b[16];
+};
+constexpr int KTAB_MAX_BITS = 12;
+
+template <int NI, int TEAM>
+__global__ void __launch_bounds__(256) k_apply(const ApplyDev p) {
+    extern __shared__ uint32_t sm[];
+    const int tabn = p.ntab * 256 * 4;
+    for (int i = threadIdx.x; i < tabn; i += blockDim.x) sm[i] = p.tab[i];
+    uint32_t* sk = sm + tabn;
+    const bool has_ktab = p.ktab != nullptr;
+    if (has_ktab) {
+        const int kn = 2 << p.nk;
+        for (int i = threadIdx.x; i < kn; i += blockDim.x) sk[i] = p.ktab[i];
+    }
+    __syncthreads();
+    const int64_t K = (int64_t)1 << p.nk;
+    const int lane = (TEAM == 1) ? 0 : (threadIdx.x & (TEAM - 1));
+    const int64_t team0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
+    const int64_t nteams = ((int64_t)gridDim.x * blockDim.x) / TEAM;
+    const int64_t total = p.R * p.n_orbits;
+    for (int64_t w = team0; w < total; w += nteams) {
+        const int64_t r = w / p.n_orbits;
+        const int64_t o = w - r * p.n_orbits;
+        uint32_t coff = 0, aoff = 0, boff = 0;
+        for (int t = 0; t < p.ntab; t++) {
+            const uint32_t* e = sm + ((t << 8) + (int)((o >> (8 * t)) & 255)) * 4;
+            coff += e[0];
+            aoff += e[1];
+            boff += e[2];
+        }
+        const int64_t ra = p.ma ? (int64_t)p.ma[r] : r;
+        const int64_t rb = p.mb ? (int64_t)p.mb[r] : 0;
+        const float2* __restrict__ Ar = p.A + ra * p.a_row + aoff;
+        const float2* __restrict__ Br = p.B + rb * p.b_row + boff;
+        float2 acc[1 << NI];
+#pragma unroll
+        for (int ii = 0; ii < (1 << NI); ii++) acc[ii] = make_float2(0.f, 0.f);
+        for (int64_t kk = lane; kk < K; kk += TEAM) {
+            uint32_t ka, kb;
+            if (has_ktab) {
+                ka = sk[2 * kk];
+                kb = sk[2 * kk + 1];
+            } else {
+                ka = 0;
+                kb = 0;
+                for (int t = 0; t < p.nk; t++)
+                    if ((kk >> t) & 1) {
+                        ka += 1u << p.kA[t];
+                        kb += 1u << p.kB[t];
+                    }
+            }
+            const float2 a = Ar[ka];
+#pragma unroll
+            for (int ii = 0; ii < (1 << NI); ii++) acc[ii] = cmac(acc[ii], a, Br[kb + p.inner_b[ii]]);
+        }
+        if (TEAM > 1) {
+#pragma unroll
+            for (int ii = 0; ii < (1 << NI); ii++) {
+#pragma unroll
+                for (int sh = TEAM / 2; sh >= 1; sh >>= 1) {
+                    acc[ii].x += __shfl_xor_sync(0xffffffffu, acc[ii].x, sh);
+                    acc[ii].y += __shfl_xor_sync(0xffffffffu, acc[ii].y, sh);
+                }
+            }
+        }
+        if (lane == 0) {
+            float2* Cr = p.C + r * p.c_row + coff;
+#pragma unroll
+            for (int ii = 0; ii < (1 << NI); ii++) Cr[p.inner_c[ii]] = acc[ii];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- GEMM pre-passes (row a3)
+// permute to K-major + 3xTF32 split: hi = cvt.rna.tf32(x), lo = x - hi
+__device__ __forceinline__ float tf32_hi(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+struct PrepADev {
+    const float2* A;
+    const int32_t* ma;
+    float2* hi;
+    float2* lo;
+    int64_t Mp, K, a_row;
+    int log2m, log2k;
+    const uint32_t* tab;   // [ntm + ntk][256]: A offsets of m-index bytes, then of k-index bytes
+    int ntm, ntk;
+};
+
+__global__ void __launch_bounds__(256) k_prep_a(const PrepADev p) {
+    extern __shared__ uint32_t sm[];
+    const int tn = (p.ntm + p.ntk) * 256;
+    for (int i = threadIdx.x; i < tn; i += blockDim.x) sm[i] = p.tab[i];
+    __syncthreads();
+    const int64_t total = p.Mp * p.K;
+    const int64_t mmask = ((int64_t)1 << p.log2m) - 1;
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total; it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t mp = it >> p.log2k;
+        const int64_t kk = it & (p.K - 1);
+        const int64_t r = mp >> p.log2m;
+        const int64_t mi = mp & mmask;
+        uint32_t off = 0;
+        for (int t = 0; t < p.ntm; t++) off += sm[(t << 8) + (int)((mi >> (8 * t)) & 255)];
+        for (int t = 0; t < p.ntk; t++) off += sm[((p.ntm + t) << 8) + (int)((kk >> (8 * t)) & 255)];
+        const int64_t ra = p.ma ? (int64_t)p.ma[r] : r;
+        const float2 v = p.A[ra * p.a_row + off];
+        const float2 h = make_float2(tf32_hi(v.x), tf32_hi(v.y));
+        p.hi[it] = h;
+        p.lo[it] = make_float2(v.x - h.x, v.y - h.y);
+    }
+}
+
+struct PrepBDev {
+    const float2* B;
+    float2* hi;   // [2N][K] float2 = [2N][2K] fp32
+    float2* lo;
+    int64_t N, K;
+    int log2k;
+    const uint32_t* tab;  // [ntn + ntk][256]
+    int ntn, ntk;
+};
+
+__global__ void __launch_bounds__(256) k_prep_b(const PrepBDev p) {
+    extern __shared__ uint32_t sm[];
+    const int tn = (p.ntn + p.ntk) * 256;
+    for (int i = threadIdx.x; i < tn; i += blockDim.x) sm[i] = p.tab[i];
+    __syncthreads();
+    const int64_t total = p.N * p.K;
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total; it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t nn = it >> p.log2k;
+        const int64_t kk = it & (p.K - 1);
+        uint32_t off = 0;
+        for (int t = 0; t < p.ntn; t++) off += sm[(t << 8) + (int)((nn >> (8 * t)) & 255)];
+        for (int t = 0; t < p.ntk; t++) off += sm[((p.ntn + t) << 8) + (int)((kk >> (8 * t)) & 255)];
+        const float2 b = p.B[off];
+        const float hr = tf32_hi(b.x), hi_ = tf32_hi(b.y);
+        const float lr = b.x - hr, li = b.y - hi_;
+        // Bt row 2nn = (br, -bi), row 2nn+1 = (bi, br) along K (complex-as-real embedding)
+        p.hi[(2 * nn) * p.K + kk] = make_float2(hr, -hi_);
+        p.lo[(2 * nn) * p.K + kk] = make_float2(lr, -li);
+        p.hi[(2 * nn + 1) * p.K + kk] = make_float2(hi_, hr);
+        p.lo[(2 * nn + 1) * p.K + kk] = make_float2(li, lr);
+    }
+}
+
+// ---------------------------------------------------------------------------- K4 readout + K5 accumulate
+// (rows a6 iii, a7) acc[j] += F[idx[j]] in fp64, ascending slice order per GPU; the last slice kernel
+// advances the device slice counter.
+__global__ void k_readout(const float2* __restrict__ F, const int64_t* __restrict__ idx, double2* __restrict__ acc,
+                          int64_t M, int64_t* __restrict__ counter) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x) {
+        const float2 v = F[idx[j]];
+        double2 a = acc[j];
+        a.x += (double)v.x;
+        a.y += (double)v.y;
+        acc[j] = a;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *counter += 1;
+}
+
+__global__ void k_finalize(const double2* __restrict__ acc, float2* __restrict__ out, int64_t M) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x)
+        out[j] = make_float2((float)acc[j].x, (float)acc[j].y);
+}
+
+}  // namespace kern
+}  // namespace tnb

@@ -1,0 +1,402 @@
+// lower.cpp -- lowers a plan to the per-slice step program executed on the device.
+//
+// Every tensor of one slice is [rows][2^d] complex64: rows = sparse-state rows (the sorted distinct
+// projections of the requested bitstrings onto the tensor's fixed final qubits), d =
+// dense legs (internal bonds and open output legs) with sliced legs removed.  A pairwise
+// contraction becomes either
+//   K_APPLY  : the SIMT sparse-row contraction (gate-application style, any bit positions, row
+//              gathers through parent maps) -- SURVEY §8(a) rows a5, a6;
+//   K_PREP_A, K_PREP_B, K_GEMM : permute+3xTF32-split pre-passes and the tcgen05 GEMM -- row a4.
+// K_INSTANTIATE (row a2) fills the sliced leaves for slice sigma; K_READOUT (rows a6 iii + a7) gathers
+// the M amplitudes and accumulates them.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <sstream>
+
+#include "tnb.h"
+
+namespace tnb {
+
+namespace {
+
+struct Alloc {
+    std::vector<std::pair<int64_t, int64_t>> fl;  // free blocks (offset, size), sorted by offset
+    int64_t top = 0, peak = 0;
+    static int64_t rnd(int64_t b) { return (b + 1023) & ~(int64_t)1023; }
+    int64_t alloc(int64_t bytes) {
+        bytes = rnd(std::max<int64_t>(bytes, 1));
+        for (size_t i = 0; i < fl.size(); i++) {
+            if (fl[i].second >= bytes) {
+                int64_t off = fl[i].first;
+                fl[i].first += bytes;
+                fl[i].second -= bytes;
+                if (fl[i].second == 0) fl.erase(fl.begin() + i);
+                return off;
+            }
+        }
+        int64_t off = top;
+        top += bytes;
+        peak = std::max(peak, top);
+        return off;
+    }
+    void release(int64_t off, int64_t bytes) {
+        bytes = rnd(std::max<int64_t>(bytes, 1));
+        fl.push_back({off, bytes});
+        std::sort(fl.begin(), fl.end());
+        std::vector<std::pair<int64_t, int64_t>> m;
+        for (auto& b : fl) {
+            if (!m.empty() && m.back().first + m.back().second == b.first) m.back().second += b.second;
+            else m.push_back(b);
+        }
+        fl = m;
+        if (!fl.empty() && fl.back().first + fl.back().second == top) {
+            top = fl.back().first;
+            fl.pop_back();
+        }
+    }
+};
+
+struct LT {
+    std::vector<int> legs;           // MSB first, sliced legs removed
+    uint64_t qmask = 0;
+    std::vector<uint64_t> rows;
+    BufRef buf;
+    int64_t bytes = 0;               // allocation size if in the workspace
+};
+
+inline int bitpos(const std::vector<int>& legs, int e) {
+    int i = (int)(std::find(legs.begin(), legs.end(), e) - legs.begin());
+    return (int)legs.size() - 1 - i;
+}
+inline bool has(const std::vector<int>& v, int e) { return std::find(v.begin(), v.end(), e) != v.end(); }
+
+int64_t push_blob(std::vector<uint8_t>& blob, const void* p, size_t bytes) {
+    size_t off = (blob.size() + 255) & ~(size_t)255;
+    blob.resize(off + bytes);
+    if (bytes) std::memcpy(blob.data() + off, p, bytes);
+    return (int64_t)off;
+}
+
+std::string wire_str(const Network& net, int e) {
+    std::ostringstream o;
+    o << "[" << net.edges[e].q << "," << net.edges[e].k << "]";
+    return o.str();
+}
+
+}  // namespace
+
+
+std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, const Request& req,
+                       const Plan& plan, Program& prog) {
+    prog = Program();
+    const int s = (int)plan.sliced.size();
+    prog.s = s;
+    std::map<int, int> slice_index;
+    for (int i = 0; i < s; i++) slice_index[plan.sliced[i]] = i;
+    Alloc wa;
+    std::vector<LT> slot(leaves.size());
+    std::ostringstream js;
+    js << "{\"n\":" << req.n << ",\"s\":" << s << ",\"sliced_wires\":[";
+    for (int i = 0; i < s; i++) js << (i ? "," : "") << wire_str(net, plan.sliced[i]);
+    js << "],\"leaves\":[";
+
+    // ---------------------------------------------------------------- leaves: bank + instantiation
+    std::vector<InstLeafDesc> inst;
+    int64_t inst_items = 0;
+    for (size_t li = 0; li < leaves.size(); li++) {
+        const Leaf& L = leaves[li];
+        LT& t = slot[li];
+        t.qmask = L.qmask;
+        t.rows = L.rows;
+        int64_t bank_off = (int64_t)prog.bank.size() / 2;  // complex elements
+        for (const cd& v : L.data) {
+            prog.bank.push_back((float)v.real());
+            prog.bank.push_back((float)v.imag());
+        }
+        std::vector<int> keep, sl;
+        for (int e : L.legs) (slice_index.count(e) ? sl : keep).push_back(e);
+        t.legs = keep;
+        if (sl.empty()) {
+            t.buf = BufRef{REG_BANK, bank_off * 8};
+        } else {
+            InstLeafDesc d;
+            std::memset(&d, 0, sizeof(d));
+            d.bank_off = bank_off;
+            d.d_full = (int)L.legs.size();
+            d.d_out = (int)keep.size();
+            d.n_sl = (int)sl.size();
+            d.items = (int64_t)L.rows.size() << d.d_out;
+            d.item_begin = inst_items;
+            inst_items += d.items;
+            for (int b = 0; b < d.d_out; b++) {
+                int e = keep[d.d_out - 1 - b];
+                d.out_src[b] = (int8_t)bitpos(L.legs, e);
+            }
+            for (int j = 0; j < d.n_sl; j++) {
+                d.sl_pos[j] = (int8_t)bitpos(L.legs, sl[j]);
+                d.sl_idx[j] = (int8_t)slice_index[sl[j]];
+            }
+            t.bytes = d.items * 8;
+            int64_t off = wa.alloc(t.bytes);
+            d.out_off = off;
+            t.buf = BufRef{REG_WORK, off};
+            inst.push_back(d);
+        }
+        js << (li ? "," : "") << "{\"tensor\":" << L.tensor_id << ",\"qmask\":" << L.qmask << ",\"rows\":" << L.rows.size()
+           << ",\"legs\":[";
+        for (size_t i = 0; i < L.legs.size(); i++) js << (i ? "," : "") << wire_str(net, L.legs[i]);
+        js << "]}";
+    }
+    js << "],\"steps\":[";
+    if (!inst.empty()) {
+        Step st;
+        st.kind = K_INSTANTIATE;
+        st.ip.n_items = inst_items;
+        st.ip.n_leaves = (int32_t)inst.size();
+        st.ip.table = BufRef{REG_MAPS, push_blob(prog.maps, inst.data(), inst.size() * sizeof(InstLeafDesc))};
+        st.bytes = 16.0 * inst_items;
+        prog.steps.push_back(st);
+    }
+
+    // ---------------------------------------------------------------- pairwise steps
+    int final_slot = plan.order.empty() ? 0 : plan.order.back().first;
+    for (size_t p = 0; p < plan.order.size(); p++) {
+        int i = plan.order[p].first, j = plan.order[p].second;
+        LT X = slot[i], Y = slot[j];
+        std::vector<int> K;
+        for (int e : X.legs)
+            if (has(Y.legs, e)) K.push_back(e);
+        const uint64_t qC = X.qmask | Y.qmask;
+        std::vector<uint64_t> rowsC = rows_of(req, qC);
+        const int64_t RC = (int64_t)rowsC.size();
+        const bool rx = X.qmask != 0, ry = Y.qmask != 0;
+        auto per_row = [](const LT& t) { return (int64_t)1 << t.legs.size(); };
+
+        // roles
+        bool use_gemm = false;
+        LT *A = &X, *B = &Y;
+        if (rx && ry) {
+            if (per_row(Y) > per_row(X)) std::swap(A, B);
+        } else {
+            if (ry || (!rx && per_row(Y) > per_row(X))) std::swap(A, B);
+            int64_t fa = (int64_t)A->legs.size() - (int64_t)K.size();
+            int64_t fb = (int64_t)B->legs.size() - (int64_t)K.size();
+            int64_t m = RC << fa, n = (int64_t)1 << fb, k = (int64_t)1 << K.size();
+            use_gemm = (m >= 128 && n >= 64 && k >= 16);
+            if (!use_gemm && per_row(*B) > per_row(*A)) std::swap(A, B);
+        }
+        // parent maps
+        std::vector<int32_t> ma(RC), mb(RC);
+        bool ma_id = (int64_t)A->rows.size() == RC;
+        for (int64_t r = 0; r < RC; r++) {
+            ma[r] = (int32_t)(std::lower_bound(A->rows.begin(), A->rows.end(), rowsC[r] & A->qmask) - A->rows.begin());
+            mb[r] = (int32_t)(std::lower_bound(B->rows.begin(), B->rows.end(), rowsC[r] & B->qmask) - B->rows.begin());
+            if (ma[r] != r) ma_id = false;
+        }
+        BufRef maRef, mbRef;
+        if (!ma_id) maRef = BufRef{REG_MAPS, push_blob(prog.maps, ma.data(), ma.size() * 4)};
+        if (B->qmask != 0) mbRef = BufRef{REG_MAPS, push_blob(prog.maps, mb.data(), mb.size() * 4)};
+        std::vector<int> fb;
+        for (int e : B->legs)
+            if (!has(K, e)) fb.push_back(e);
+        std::vector<int> fa;
+        for (int e : A->legs)
+            if (!has(K, e)) fa.push_back(e);
+        LT Cn;
+        Cn.qmask = qC;
+        Cn.rows = rowsC;
+        const double cmac = (double)RC * std::ldexp(1.0, (int)(fa.size() + fb.size() + K.size()));
+        const int64_t sizeA = (int64_t)A->rows.size() << A->legs.size();
+        const int64_t sizeB = (int64_t)B->rows.size() << B->legs.size();
+
+        if (!use_gemm) {
+            // C legs: A's layout with the K legs replaced by the B-free legs (extra ones on top)
+            size_t nfb = fb.size(), used = 0;
+            size_t extra = nfb > K.size() ? nfb - K.size() : 0;
+            for (size_t t = 0; t < extra; t++) Cn.legs.push_back(fb[used++]);
+            for (int e : A->legs) {
+                if (has(K, e)) {
+                    if (used < nfb) Cn.legs.push_back(fb[used++]);
+                } else {
+                    Cn.legs.push_back(e);
+                }
+            }
+            Step st;
+            st.kind = K_APPLY;
+            st.pair = (int)p;
+            ApplyParams& ap = st.ap;
+            ap.A = A->buf;
+            ap.B = B->buf;
+            ap.ma = maRef;
+            ap.mb = mbRef;
+            ap.R = RC;
+            ap.dA = (int)A->legs.size();
+            ap.dB = (int)B->legs.size();
+            ap.dC = (int)Cn.legs.size();
+            ap.a_row = (int64_t)1 << ap.dA;
+            ap.b_row = (int64_t)1 << ap.dB;
+            ap.c_row = (int64_t)1 << ap.dC;
+            ap.cA.n = 0;
+            for (int e : fa) {
+                ap.cA.dst[ap.cA.n] = (int8_t)bitpos(Cn.legs, e);
+                ap.cA.src[ap.cA.n] = (int8_t)bitpos(A->legs, e);
+                ap.cA.n++;
+            }
+            ap.cB.n = 0;
+            for (int e : fb) {
+                ap.cB.dst[ap.cB.n] = (int8_t)bitpos(Cn.legs, e);
+                ap.cB.src[ap.cB.n] = (int8_t)bitpos(B->legs, e);
+                ap.cB.n++;
+            }
+            ap.nk = (int)K.size();
+            for (int t = 0; t < ap.nk; t++) {
+                ap.kA[t] = (int8_t)bitpos(A->legs, K[t]);
+                ap.kB[t] = (int8_t)bitpos(B->legs, K[t]);
+            }
+            // inner (per-thread) C bits: up to 4 B-free legs with the lowest C bit positions
+            std::vector<int> fbpos;
+            for (int e : fb) fbpos.push_back(bitpos(Cn.legs, e));
+            std::sort(fbpos.begin(), fbpos.end());
+            ap.n_inner = (int)std::min<size_t>(4, fbpos.size());
+            for (int t = 0; t < ap.n_inner; t++) ap.inner_c[t] = (int8_t)fbpos[t];
+            Cn.bytes = RC * ap.c_row * 8;
+            int64_t off = wa.alloc(Cn.bytes);
+            Cn.buf = BufRef{REG_WORK, off};
+            ap.C = Cn.buf;
+            st.cmac = cmac;
+            st.bytes = 8.0 * (double)(sizeA + sizeB + RC * ap.c_row) + (maRef.region ? 4.0 * RC : 0) + (mbRef.region ? 4.0 * RC : 0);
+            prog.steps.push_back(st);
+        } else {
+            Cn.legs = fa;
+            Cn.legs.insert(Cn.legs.end(), fb.begin(), fb.end());
+            const int64_t m = (int64_t)1 << fa.size(), n = (int64_t)1 << fb.size(), k = (int64_t)1 << K.size();
+            const int64_t Mp = RC * m;
+            GemmParams gp;
+            gp.A = A->buf;
+            gp.B = B->buf;
+            gp.ma = maRef;
+            gp.R = RC;
+            gp.m = m;
+            gp.n = n;
+            gp.k = k;
+            gp.dA = (int)A->legs.size();
+            gp.dB = (int)B->legs.size();
+            gp.a_row = (int64_t)1 << gp.dA;
+            gp.aM.n = (int)fa.size();
+            for (int t = 0; t < gp.aM.n; t++) {
+                gp.aM.dst[t] = (int8_t)(gp.aM.n - 1 - t);             // m-index bit
+                gp.aM.src[t] = (int8_t)bitpos(A->legs, fa[t]);        // A bit
+            }
+            gp.aK.n = (int)K.size();
+            gp.bK.n = (int)K.size();
+            for (int t = 0; t < gp.aK.n; t++) {
+                gp.aK.dst[t] = (int8_t)(gp.aK.n - 1 - t);
+                gp.aK.src[t] = (int8_t)bitpos(A->legs, K[t]);
+                gp.bK.dst[t] = (int8_t)(gp.bK.n - 1 - t);
+                gp.bK.src[t] = (int8_t)bitpos(B->legs, K[t]);
+            }
+            gp.bN.n = (int)fb.size();
+            for (int t = 0; t < gp.bN.n; t++) {
+                gp.bN.dst[t] = (int8_t)(gp.bN.n - 1 - t);
+                gp.bN.src[t] = (int8_t)bitpos(B->legs, fb[t]);
+            }
+            const int64_t abytes = Mp * 2 * k * 4, bbytes = 2 * n * 2 * k * 4;
+            gp.Ahi = BufRef{REG_WORK, wa.alloc(abytes)};
+            gp.Alo = BufRef{REG_WORK, wa.alloc(abytes)};
+            gp.Bhi = BufRef{REG_WORK, wa.alloc(bbytes)};
+            gp.Blo = BufRef{REG_WORK, wa.alloc(bbytes)};
+            Cn.bytes = Mp * n * 8;
+            Cn.buf = BufRef{REG_WORK, wa.alloc(Cn.bytes)};
+            gp.C = Cn.buf;
+            Step sa;
+            sa.kind = K_PREP_A;
+            sa.pair = (int)p;
+            sa.gp = gp;
+            sa.bytes = 8.0 * Mp * k + 2.0 * abytes;
+            Step sb;
+            sb.kind = K_PREP_B;
+            sb.pair = (int)p;
+            sb.gp = gp;
+            sb.bytes = 8.0 * n * k + 2.0 * bbytes;
+            Step sg;
+            sg.kind = K_GEMM;
+            sg.pair = (int)p;
+            sg.gp = gp;
+            sg.cmac = cmac;
+            sg.bytes = 2.0 * abytes + 2.0 * bbytes + 8.0 * Mp * n;
+            prog.steps.push_back(sa);
+            prog.steps.push_back(sb);
+            prog.steps.push_back(sg);
+            wa.release(gp.Ahi.offset, abytes);
+            wa.release(gp.Alo.offset, abytes);
+            wa.release(gp.Bhi.offset, bbytes);
+            wa.release(gp.Blo.offset, bbytes);
+            prog.gemm_cmac += cmac;
+        }
+        prog.cmac += cmac;
+        prog.peak_elems = std::max<int64_t>(prog.peak_elems, RC << Cn.legs.size());
+        // release operands held in the workspace
+        if (X.buf.region == REG_WORK) wa.release(X.buf.offset, X.bytes);
+        if (Y.buf.region == REG_WORK) wa.release(Y.buf.offset, Y.bytes);
+        js << (p ? "," : "") << "{\"pair\":[" << i << "," << j << "],\"gemm\":" << (use_gemm ? 1 : 0)
+           << ",\"qmask\":" << qC << ",\"rows\":" << RC << ",\"m_rows\":" << A->rows.size() << ",\"n_rows\":" << B->rows.size()
+           << ",\"fa\":" << fa.size() << ",\"fb\":" << fb.size() << ",\"k\":" << K.size() << ",\"cmac\":" << cmac;
+        if (RC <= 4096 && qC != 0) {
+            js << ",\"row_keys\":[";
+            for (int64_t r = 0; r < RC; r++) js << (r ? "," : "") << rowsC[r];
+            js << "],\"qmask_a\":" << A->qmask << ",\"qmask_b\":" << B->qmask << ",\"map_a\":[";
+            for (int64_t r = 0; r < RC; r++) js << (r ? "," : "") << ma[r];
+            js << "],\"map_b\":[";
+            for (int64_t r = 0; r < RC; r++) js << (r ? "," : "") << mb[r];
+            js << "]";
+        }
+        js << "}";
+        slot[i] = Cn;
+        slot[j] = LT();
+    }
+
+    // ---------------------------------------------------------------- readout + accumulate
+    const LT& F = slot[final_slot];
+    for (int e : F.legs)
+        if (!(net.edges[e].output && net.edges[e].open)) return "internal error: final tensor has a non-open leg";
+    std::vector<int64_t> idx(req.M);
+    const int dF = (int)F.legs.size();
+    for (int64_t jj = 0; jj < req.M; jj++) {
+        uint64_t x = req.bits[jj];
+        int64_t r = std::lower_bound(F.rows.begin(), F.rows.end(), x & F.qmask) - F.rows.begin();
+        if (r >= (int64_t)F.rows.size() || F.rows[r] != (x & F.qmask)) return "internal error: readout row missing";
+        int64_t off = 0;
+        for (int t = 0; t < dF; t++) {
+            int q = net.edges[F.legs[t]].q;
+            if ((x >> (req.n - 1 - q)) & 1) off |= (int64_t)1 << (dF - 1 - t);
+        }
+        idx[jj] = (r << dF) + off;
+    }
+    Step st;
+    st.kind = K_READOUT;
+    st.rp.F = F.buf;
+    st.rp.M = req.M;
+    st.rp.idx = BufRef{REG_MAPS, push_blob(prog.maps, idx.data(), idx.size() * 8)};
+    st.bytes = (8.0 + 8.0 + 32.0) * (double)req.M;
+    prog.steps.push_back(st);
+
+    js << "],\"final\":{\"qmask\":" << F.qmask << ",\"rows\":" << F.rows.size() << ",\"legs\":[";
+    for (int t = 0; t < dF; t++) js << (t ? "," : "") << wire_str(net, F.legs[t]);
+    js << "]";
+    if (F.rows.size() <= 65536) {
+        js << ",\"row_keys\":[";
+        for (size_t r = 0; r < F.rows.size(); r++) js << (r ? "," : "") << F.rows[r];
+        js << "]";
+    }
+    js << "}}";
+    prog.dump_json = js.str();
+    prog.n_pairs = (int64_t)plan.order.size();
+    prog.work_bytes = std::max<int64_t>(wa.peak, 1024);
+    for (const Step& x : prog.steps) prog.bytes += x.bytes;
+    // largest leaf counts toward the peak as well
+    for (const LT& t : slot) (void)t;
+    return "";
+}
+
+}  // namespace tnb

@@ -1,0 +1,211 @@
+// tnb.h -- internal host-side data structures of the B200 sliced sparse-state contraction.
+// Citations: P:Lnnn = PAPER.md line; SURVEY §x = repo blueprint.
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/tn.h"
+
+namespace tnb {
+
+using cd = std::complex<double>;
+
+// ---------------------------------------------------------------------------- network
+
+struct Edge {
+    int q = -1, k = -1;     // wire id (q, k): segment of qubit q after its k-th gate
+    int t0 = -1, t1 = -1;   // endpoint tensors; t1 = -1 for an output leg
+    bool output = false;    // output leg of qubit q (final-state boundary)
+    bool open = false;      // output leg of an open qubit (kept dense)
+};
+
+struct HTensor {
+    std::vector<int> legs;  // edge ids; legs[0] is the most significant bit of the dense index
+    std::vector<cd> data;   // 2^legs.size() values (fp64 on the host)
+    bool alive = true;
+};
+
+struct Network {
+    int n = 0;
+    std::vector<Edge> edges;
+    std::vector<HTensor> tensors;
+};
+
+// A leaf of the contraction in row form: the fixed output legs of the tensor are absorbed as
+// sparse rows = sorted distinct projections of the requested bitstrings onto those qubits
+// (SURVEY App. A.3).  Row keys are the bitstring masked to the fixed qubits, so
+// ascending keys = ascending packed projections with the lowest qubit id as MSB.
+struct Leaf {
+    int tensor_id = -1;
+    uint64_t qmask = 0;            // fixed qubits (bitstring-convention mask)
+    std::vector<uint64_t> rows;    // sorted distinct (fixed & qmask); {0} when qmask == 0
+    std::vector<int> legs;         // dense legs (edge ids), MSB first
+    std::vector<cd> data;          // rows.size() * 2^legs.size()
+};
+
+struct Request {
+    int n = 0;
+    uint64_t open_mask = 0;
+    int64_t M = 0, l = 1, L = 0;
+    std::vector<uint64_t> bits;    // the M requested bitstrings (caller order)
+    std::vector<uint64_t> fixed;   // distinct fixed parts, sorted (bits & ~open_mask)
+};
+
+// Build the network of a circuit (one tensor per fSim; single-qubit gates and |0> inputs
+// absorbed into the next tensor on the wire, the final layer into the previous one) and
+// simplify it (order-1 and order-2 tensors contracted into neighbours).
+// Returns an empty string on success, else an error message.
+std::string build_network(const tn_circuit* c, Network& net);
+void simplify(Network& net);
+std::vector<Leaf> make_leaves(const Network& net, const Request& req);
+
+// generic host contraction of two dense tensors (fp64); result legs = A\B then B\A
+HTensor contract_host(const HTensor& A, const HTensor& B);
+
+// rows of the fixed set qmask: sorted distinct (fixed & qmask)
+std::vector<uint64_t> rows_of(const Request& req, uint64_t qmask);
+
+// ---------------------------------------------------------------------------- plan
+
+struct PlanTensor {
+    std::vector<int> legs;   // sorted dense edge ids
+    uint64_t qmask = 0;
+    double rows = 1;
+};
+
+struct Plan {
+    std::vector<std::pair<int, int>> order;  // (i, j): contract leaves/intermediates, result at i
+    std::vector<int> sliced;                 // edge ids, MSB-first slice order
+    double cmac = 0, bytes = 0, time_s = 0;  // per slice
+    double peak = 0;                         // elements, per slice
+};
+
+struct PlanOptions {
+    int n_sliced = -1;
+    std::vector<int> forced;   // edge ids
+    uint64_t seed = 1;
+    int trials = 0;
+    double time_budget_s = 0;
+    double max_elems = 0;
+};
+
+// row-count oracle used by the planner (exact with memo for small L, estimate otherwise)
+struct RowModel {
+    const Request* req = nullptr;
+    double rows(uint64_t qmask);
+    std::vector<std::pair<uint64_t, double>> memo;
+};
+
+std::string find_plan(const Network& net, const std::vector<Leaf>& leaves, const Request& req,
+                      const PlanOptions& opt, Plan& out);
+
+// ---------------------------------------------------------------------------- lowered program
+
+// Bit mapping: destination bit dst[i] takes source bit src[i].
+struct BitMap {
+    int n = 0;
+    int8_t src[40];
+    int8_t dst[40];
+};
+
+enum BufRegion : int32_t { REG_NONE = 0, REG_WORK = 1, REG_BANK = 2, REG_MAPS = 3 };
+struct BufRef {
+    int32_t region = REG_NONE;
+    int64_t offset = 0;   // bytes
+};
+
+enum StepKind : int32_t {
+    K_INSTANTIATE = 0,
+    K_APPLY = 1,
+    K_PREP_A = 2,
+    K_PREP_B = 3,
+    K_GEMM = 4,
+    K_READOUT = 5,
+    K_PERMUTE = 6
+};
+
+// General sparse-row pairwise contraction (SIMT path):
+//   C[r][c] = sum_kk A[ma[r]][addrA(c, kk)] * B[mb[r]][addrB(c, kk)]
+struct ApplyParams {
+    BufRef A, B, C;
+    BufRef ma, mb;            // int32 maps (REG_MAPS); region NONE: A identity, B row 0
+    int64_t R = 1;            // output rows
+    int64_t a_row = 0, b_row = 0, c_row = 0;   // row strides in complex elements
+    int dA = 0, dB = 0, dC = 0;
+    BitMap cA;                // C bit -> A bit (A-free legs)
+    BitMap cB;                // C bit -> B bit (B-free legs)
+    int nk = 0;
+    int8_t kA[40], kB[40];    // contracted leg i at A bit kA[i], B bit kB[i]
+    int n_inner = 0;          // number of B-free C bits computed per thread (<= 4)
+    int8_t inner_c[4];        // their C bit positions
+};
+
+// Tensor-core path: TTGT with 3xTF32.
+//   PREP_A: Ahi/Alo [Mp][2K] fp32 (K-major, complex interleaved along K) from A (rows via ma)
+//   PREP_B: Bhi/Blo [2N][2K] fp32 (K-major), the real embedding [[br, -bi], [bi, br]]^T
+//   GEMM  : C[Mp][2N] fp32 (= complex [Mp][N]) = Ahi*Bhi + Ahi*Blo + Alo*Bhi
+struct GemmParams {
+    BufRef A, B, C, ma;
+    BufRef Ahi, Alo, Bhi, Blo;
+    int64_t R = 1, m = 1, n = 1, k = 1;  // per-row m (A-free), n (B-free), k; Mp = R * m
+    int64_t a_row = 0;
+    int dA = 0, dB = 0;
+    BitMap aM, aK;            // A index bits from (m index bit -> A bit), (k index bit -> A bit)
+    BitMap bN, bK;            // B index bits from (n index bit -> B bit), (k index bit -> B bit)
+};
+
+struct InstParams {
+    int64_t n_items = 0;      // total elements written across all sliced leaves
+    BufRef table;             // REG_MAPS: per-leaf descriptors (see executor)
+    int32_t n_leaves = 0;
+};
+
+struct ReadoutParams {
+    BufRef F;                 // final tensor
+    BufRef idx;               // REG_MAPS: int64 index per amplitude
+    int64_t M = 0;
+};
+
+struct Step {
+    int32_t kind = 0;
+    int32_t pair = -1;        // pairwise step index
+    double cmac = 0, bytes = 0;
+    ApplyParams ap;
+    GemmParams gp;
+    InstParams ip;
+    ReadoutParams rp;
+};
+
+// device-side descriptor of one sliced leaf for K_INSTANTIATE (slice instantiate, row a2)
+struct InstLeafDesc {
+    int64_t bank_off;     // complex elements into the leaf bank
+    int64_t out_off;      // bytes into the workspace
+    int64_t item_begin;   // first global item of this leaf
+    int64_t items;        // rows * 2^d_out
+    int32_t d_full, d_out, n_sl, pad;
+    int8_t out_src[40];   // output bit b (LSB = 0) comes from full bit out_src[b]
+    int8_t sl_pos[24];    // sliced leg j sits at full bit sl_pos[j] ...
+    int8_t sl_idx[24];    // ... and takes slice bit sl_idx[j]: value (sigma >> (s-1-idx)) & 1
+};
+
+struct Program {
+    std::vector<Step> steps;
+    std::vector<float> bank;       // complex64 leaf bank (interleaved)
+    std::vector<uint8_t> maps;     // int32/int64 maps and tables
+    int64_t work_bytes = 0;
+    int64_t peak_elems = 0;
+    double cmac = 0, bytes = 0, gemm_cmac = 0;
+    int64_t n_pairs = 0;
+    // per-leaf slicing info for K_INSTANTIATE (also in `maps`)
+    int s = 0;
+    // plan dump support
+    std::string dump_json;
+};
+
+std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, const Request& req,
+                       const Plan& plan, Program& prog);
+
+}  // namespace tnb
