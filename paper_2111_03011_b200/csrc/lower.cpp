@@ -97,6 +97,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     Alloc wa;
     std::vector<LT> slot(leaves.size());
     std::ostringstream js;
+    js.precision(17);
     js << "{\"n\":" << req.n << ",\"s\":" << s << ",\"sliced_wires\":[";
     for (int i = 0; i < s; i++) js << (i ? "," : "") << wire_str(net, plan.sliced[i]);
     js << "],\"leaves\":[";
