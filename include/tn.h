@@ -111,7 +111,8 @@ typedef struct {
 
 /* tn_plan -- P:L91 (complexity-greedy contraction order), P:L246 (slicing: fix index values so
  * that the space fits the device; the sum over sub-tasks returns the original contraction).
- * max_tensor_size: bound on every intermediate of one slice, in complex elements.
+ * max_tensor_size: bound on every intermediate of one slice, in complex elements (<= 2^60 for planning;
+ * tn_bind_device accepts plans whose tensors are <= 2^32 elements).
  * Fills *info (pointers owned by the ctx, valid until the next tn_plan or tn_destroy).
  * EINFEASIBLE if the bound cannot be met; EINVAL if called before tn_build or with bad forced
  * wires. */

@@ -119,7 +119,7 @@ tn_status tn_plan(tn_ctx* ctx, const tn_slicing* slicing, int64_t max_tensor_siz
     if (!ctx) return TN_EINVAL;
     if (ctx->leaves.empty()) return fail(ctx, TN_EINVAL, "tn_plan before a successful tn_build");
     if (max_tensor_size < 1) return fail(ctx, TN_EINVAL, "max_tensor_size must be >= 1");
-    if (max_tensor_size > (1ll << 32)) return fail(ctx, TN_EINVAL, "max_tensor_size must be <= 2^32");
+    if (max_tensor_size > (1ll << 60)) return fail(ctx, TN_EINVAL, "max_tensor_size must be <= 2^60");
     if (ctx->dev) {
         tnb::dev_destroy(ctx->dev);
         ctx->dev = nullptr;
@@ -195,6 +195,9 @@ tn_status tn_plan_dump(const tn_ctx* ctx, const char* path) {
 tn_status tn_bind_device(tn_ctx* ctx, int device, void* workspace, size_t bytes, void* cuda_stream) {
     if (!ctx) return TN_EINVAL;
     if (!ctx->planned) return fail(ctx, TN_EINVAL, "tn_bind_device before tn_plan");
+    if (ctx->prog.peak_elems > (1ll << 32))
+        return fail(ctx, TN_EINVAL, "plan has a tensor above 2^32 elements (executor index range); re-plan with a "
+                                    "smaller max_tensor_size");
     if (ctx->dev) {
         tnb::dev_destroy(ctx->dev);
         ctx->dev = nullptr;
