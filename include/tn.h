@@ -141,7 +141,8 @@ tn_status tn_contract(tn_ctx* ctx, const uint64_t* slice_ids, int64_t n_ids, voi
  * launch on the bound stream, no graph).  Fills up to max_stats entries. */
 typedef struct {
     int32_t kind;        /* 0 instantiate, 1 apply (SIMT contraction), 2 gemm pre-pass A,
-                            3 gemm pre-pass B, 4 tcgen05 gemm, 5 readout+accumulate, 6 permute */
+                            3 gemm pre-pass B, 4 tcgen05 gemm, 5 readout+accumulate, 6 permute,
+                            7 fused run of small steps (one persistent launch) */
     int32_t step;        /* pairwise step index (-1 for non-step launches)                    */
     double cmac;         /* complex MACs of the launch                                         */
     double bytes;        /* algorithmic bytes of the launch                                    */

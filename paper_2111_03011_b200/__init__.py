@@ -23,7 +23,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtnb200.so")
 
 TN_OK, TN_EINVAL, TN_EINFEASIBLE, TN_ENUMERIC, TN_ECUDA, TN_ENOMEM = 0, 2, 3, 4, 5, 6
-KIND_NAMES = {0: "instantiate", 1: "apply", 2: "prep_a", 3: "prep_b", 4: "gemm_tcgen05", 5: "readout", 6: "permute"}
+KIND_NAMES = {0: "instantiate", 1: "apply", 2: "prep_a", 3: "prep_b", 4: "gemm_tcgen05", 5: "readout", 6: "permute",
+              7: "multi"}
 
 
 class TnError(RuntimeError):
@@ -204,15 +205,21 @@ class SparseState:
         return {"tensors": a.value, "edges": b.value, "internal_edges": c.value}
 
     # -------------------------------------------------------------- device
-    def bind(self, device: int = 0, workspace=None, stream=None):
+    def bind(self, device: int = 0, workspace=None, stream=None, pipelines: int = 4):
         """tn_bind_device.  workspace: a torch uint8 CUDA tensor (allocated here from torch's caching
-        allocator when None); stream: a torch.cuda.Stream (current stream when None)."""
+        allocator when None, room for `pipelines` concurrent slice pipelines, capped by free memory);
+        stream: a torch.cuda.Stream (current stream when None).  The library runs
+        floor(workspace bytes / per-pipeline workspace) slice pipelines concurrently (at most 8)."""
         import torch
         if self.info is None:
             raise TnError(TN_EINVAL, "bind before plan")
         dev = torch.device("cuda", device)
         if workspace is None:
-            workspace = torch.empty(max(1, self.info["workspace_bytes"]), dtype=torch.uint8, device=dev)
+            wb = (max(1, self.info["workspace_bytes"]) + 4095) // 4096 * 4096
+            free, _ = torch.cuda.mem_get_info(dev)
+            p = max(1, min(int(pipelines), int(0.6 * free) // wb))
+            workspace = torch.empty(wb * p, dtype=torch.uint8, device=dev)
+            self.pipelines = p
         self._work = workspace
         st = stream if stream is not None else torch.cuda.current_stream(dev)
         self._stream = st

@@ -92,27 +92,47 @@ struct Launch {
     const float2* F = nullptr;
     const int64_t* ridx = nullptr;
     int64_t M = 0;
+    // operand extents in bytes (apply), for the megakernel's hazard analysis
+    int64_t a_bytes = 0, b_bytes = 0, c_bytes = 0;
+    // multi (small-step megakernel)
+    size_t m_first = 0;          // index into Device::msteps_host
+    int m_n = 0;
+    int64_t m_items = 0;
+    size_t m_sync = 0;           // int offset into Device::sync
 };
 
 }  // namespace
 
-struct Device {
-    int dev = 0;
-    cudaStream_t user = nullptr, stream = nullptr;
-    char* bank = nullptr;
-    char* maps = nullptr;
+// One slice pipeline: its own workspace, stream, CUDA graph, slice counter and fp64 accumulator.
+// Several pipelines run different slices concurrently so that one slice's latency-bound small steps
+// overlap another slice's tensor-core GEMMs.
+struct Pipe {
+    cudaStream_t stream = nullptr;
     char* work = nullptr;
-    bool own_work = false;
     uint32_t* tables = nullptr;
     double2* acc = nullptr;
-    float2* out = nullptr;
+    int64_t* counter = nullptr;
     uint64_t* slice_ids = nullptr;
     int64_t slice_cap = 0;
-    int64_t* counter = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t gexec = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evu = nullptr;
+    cudaEvent_t done = nullptr;
     std::vector<Launch> launches;
+    std::vector<kern::MStep> msteps_host;
+    kern::MStep* msteps = nullptr;
+    int* sync = nullptr;
+};
+
+struct Device {
+    int dev = 0;
+    cudaStream_t user = nullptr;
+    char* bank = nullptr;
+    char* maps = nullptr;
+    char* work_all = nullptr;
+    bool own_work = false;
+    float2* out = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evu = nullptr;
+    std::vector<Pipe> pipes;
     int64_t M = 0;
     int s = 0;
 };
@@ -150,11 +170,11 @@ int set_smem_attrs(std::string& err) {
     return TN_OK;
 }
 
-void do_launch(Device* d, const Launch& L, cudaStream_t st) {
+void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
     switch (L.kind) {
         case K_INSTANTIATE:
             kern::k_instantiate<<<L.grid, L.block, 0, st>>>(L.itab, L.in_leaves, L.in_items, (const float2*)d->bank,
-                                                            d->work, d->slice_ids, d->counter, d->s);
+                                                            P.work, P.slice_ids, P.counter, d->s);
             break;
         case K_APPLY:
             if (L.team == 32) launch_apply_ni<32>(L, st);
@@ -170,9 +190,113 @@ void do_launch(Device* d, const Launch& L, cudaStream_t st) {
             tc::k_gemm_tf32x3<<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp, L.gN2, L.gK2);
             break;
         case K_READOUT:
-            kern::k_readout<<<L.grid, L.block, 0, st>>>(L.F, L.ridx, d->acc, L.M, d->counter);
+            kern::k_readout<<<L.grid, L.block, 0, st>>>(L.F, L.ridx, P.acc, L.M, P.counter);
+            break;
+        case K_MULTI:
+            cudaMemsetAsync(P.sync + L.m_sync, 0, (size_t)(L.m_n + 1) * sizeof(int), st);
+            kern::k_multi<<<L.grid, L.block, 0, st>>>(P.msteps + L.m_first, L.m_n, L.m_items, P.sync + L.m_sync);
             break;
     }
+}
+
+// Fuse runs of consecutive small K_APPLY launches into K_MULTI launches (see kern::k_multi).
+std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
+    auto small = [](const Launch& L) {
+        return L.kind == K_APPLY && L.ap.ktab != nullptr && L.ap.R * L.ap.n_orbits <= 65536 && L.cmac <= 4.0e6;
+    };
+    auto ov = [](const void* a, int64_t na, const void* b, int64_t nb) {
+        const char* x = (const char*)a;
+        const char* y = (const char*)b;
+        return x < y + nb && y < x + na;
+    };
+    std::vector<Launch> out;
+    size_t i = 0;
+    size_t sync_off = 0;
+    while (i < in.size()) {
+        if (!small(in[i])) {
+            out.push_back(in[i++]);
+            continue;
+        }
+        size_t j = i;
+        std::vector<kern::MStep> run;
+        int64_t items = 0;
+        while (j < in.size() && small(in[j]) && run.size() < 1024) {
+            const Launch& L = in[j];
+            kern::MStep m;
+            std::memset(&m, 0, sizeof(m));
+            m.A = L.ap.A;
+            m.B = L.ap.B;
+            m.C = L.ap.C;
+            m.ma = L.ap.ma;
+            m.mb = L.ap.mb;
+            m.a_row = L.ap.a_row;
+            m.b_row = L.ap.b_row;
+            m.c_row = L.ap.c_row;
+            m.n_orbits = L.ap.n_orbits;
+            m.total = L.ap.R * L.ap.n_orbits;
+            m.tab = L.ap.tab;
+            m.ktab = L.ap.ktab;
+            m.ntab = L.ap.ntab;
+            m.nk = L.ap.nk;
+            m.ni = L.ni;
+            for (int t = 0; t < 16; t++) {
+                m.inner_c[t] = L.ap.inner_c[t];
+                m.inner_b[t] = L.ap.inner_b[t];
+            }
+            m.chunks = (int)((m.total + 255) / 256);
+            m.item_begin = items;
+            // hazards against earlier steps of the run
+            std::vector<int> deps;
+            for (int t = 0; t < (int)run.size(); t++) {
+                const Launch& P = in[i + t];
+                bool h = ov(L.ap.A, L.a_bytes, P.ap.C, P.c_bytes) || ov(L.ap.B, L.b_bytes, P.ap.C, P.c_bytes) ||
+                         ov(L.ap.C, L.c_bytes, P.ap.A, P.a_bytes) || ov(L.ap.C, L.c_bytes, P.ap.B, P.b_bytes) ||
+                         ov(L.ap.C, L.c_bytes, P.ap.C, P.c_bytes);
+                if (h) deps.push_back(t);
+            }
+            // transitive reduction: drop t if a later dep u already depends on t
+            std::vector<int> red;
+            for (int t : deps) {
+                bool implied = false;
+                for (int u : deps) {
+                    if (u <= t) continue;
+                    for (int k = 0; k < run[u].ndep; k++)
+                        if (run[u].dep[k] == t) implied = true;
+                }
+                if (!implied) red.push_back(t);
+            }
+            if ((int)red.size() > kern::MULTI_MAX_DEPS) break;
+            m.ndep = (int)red.size();
+            for (int k = 0; k < m.ndep; k++) m.dep[k] = red[k];
+            items += m.chunks;
+            run.push_back(m);
+            j++;
+        }
+        if (run.size() < 2) {
+            out.push_back(in[i]);
+            i = i + 1;
+            continue;
+        }
+        Launch M;
+        M.kind = K_MULTI;
+        M.pair = in[i].pair;
+        for (size_t t = i; t < j; t++) {
+            M.cmac += in[t].cmac;
+            M.bytes += in[t].bytes;
+        }
+        M.m_first = P.msteps_host.size();
+        M.m_n = (int)run.size();
+        M.m_items = items;
+        M.m_sync = sync_off;
+        sync_off += run.size() + 1;
+        M.rows = (int64_t)run.size();
+        M.block = dim3(256);
+        M.grid = dim3((unsigned)std::min<int64_t>(items, 148 * 4));
+        P.msteps_host.insert(P.msteps_host.end(), run.begin(), run.end());
+        out.push_back(M);
+        i = j;
+    }
+    return out;
 }
 
 dim3 grid_for(int64_t threads, int64_t per_block = 256, int64_t cap = 148 * 16) {
@@ -183,76 +307,19 @@ dim3 grid_for(int64_t threads, int64_t per_block = 256, int64_t cap = 148 * 16) 
 
 }  // namespace
 
-int dev_bind(Device** out, const Program& prog, int device, void* workspace, size_t bytes, void* stream, int64_t M,
-             std::string& err) {
-    *out = nullptr;
-    Device* d = new Device();
-    auto fail = [&](int code) {
-        dev_destroy(d);
-        return code;
-    };
-    d->dev = device;
-    d->M = M;
-    d->s = prog.s;
-    if (cudaSetDevice(device) != cudaSuccess) {
-        err = "cudaSetDevice failed (no GPU?)";
-        delete d;
-        return TN_ECUDA;
-    }
-    {
-        int rc = set_smem_attrs(err);
-        if (rc) return fail(rc);
-    }
-    d->user = (cudaStream_t)stream;
-#define CKF(x)                                                                   \
-    do {                                                                         \
-        cudaError_t e_ = (x);                                                    \
-        if (e_ != cudaSuccess) {                                                 \
-            err = std::string(#x) + " failed: " + cudaGetErrorString(e_);        \
-            return fail(TN_ECUDA);                                               \
-        }                                                                        \
-    } while (0)
-    CKF(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
-    CKF(cudaEventCreate(&d->ev0));
-    CKF(cudaEventCreate(&d->ev1));
-    CKF(cudaEventCreateWithFlags(&d->evu, cudaEventDisableTiming));
-    if (workspace) {
-        if ((int64_t)bytes < prog.work_bytes) {
-            std::ostringstream o;
-            o << "workspace too small: need " << prog.work_bytes << " bytes, got " << bytes;
-            err = o.str();
-            return fail(TN_ENOMEM);
-        }
-        d->work = (char*)workspace;
-    } else {
-        if (cudaMalloc(&d->work, prog.work_bytes) != cudaSuccess) {
-            err = "cudaMalloc(workspace) failed";
-            return fail(TN_ENOMEM);
-        }
-        d->own_work = true;
-    }
-    CKF(cudaMalloc(&d->bank, std::max<size_t>(prog.bank.size() * 4, 16)));
-    CKF(cudaMemcpy(d->bank, prog.bank.data(), prog.bank.size() * 4, cudaMemcpyHostToDevice));
-    CKF(cudaMalloc(&d->maps, std::max<size_t>(prog.maps.size(), 16)));
-    if (!prog.maps.empty()) CKF(cudaMemcpy(d->maps, prog.maps.data(), prog.maps.size(), cudaMemcpyHostToDevice));
-    CKF(cudaMalloc(&d->acc, std::max<int64_t>(M, 1) * sizeof(double2)));
-    CKF(cudaMalloc(&d->out, std::max<int64_t>(M, 1) * sizeof(float2)));
-    CKF(cudaMalloc(&d->counter, sizeof(int64_t)));
-    d->slice_cap = 1024;
-    CKF(cudaMalloc(&d->slice_ids, d->slice_cap * sizeof(uint64_t)));
-    CKF(cudaMemset(d->slice_ids, 0, d->slice_cap * sizeof(uint64_t)));
-    CKF(cudaMemset(d->counter, 0, sizeof(int64_t)));
+namespace {
 
+// Resolve the step program into launches for pipeline P (workspace base P.work), fuse small steps,
+// upload its tables and capture its per-slice graph.
+int build_pipe(Device* d, Pipe& P, const Program& prog, std::string& err) {
     auto ptr = [&](const BufRef& b) -> char* {
         switch (b.region) {
-            case REG_WORK: return d->work + b.offset;
+            case REG_WORK: return P.work + b.offset;
             case REG_BANK: return d->bank + b.offset;
             case REG_MAPS: return d->maps + b.offset;
             default: return nullptr;
         }
     };
-
-    // ---------------------------------------------------------------- index tables (host build)
     std::vector<uint32_t> tabs;  // concatenated; offsets recorded per launch (in uint32 units)
     struct TabFix { size_t launch; int which; size_t off; };
     std::vector<TabFix> fixes;
@@ -309,6 +376,7 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
                 p.inner_b[ii] = bo;
             }
             L.ni = a.n_inner;
+            tabs.resize((tabs.size() + 3) & ~(size_t)3, 0);
             size_t base = tabs.size();
             tabs.resize(base + (size_t)std::max(p.ntab, 0) * 256 * 4, 0);
             {
@@ -324,9 +392,10 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
                 push_tables(tmp, bb, 4, 2);
                 std::copy(tmp.begin(), tmp.end(), tabs.begin() + base);
             }
-            fixes.push_back({d->launches.size(), 0, base});
+            fixes.push_back({P.launches.size(), 0, base});
             size_t kbase = 0;
             if (a.nk <= kern::KTAB_MAX_BITS) {
+                tabs.resize((tabs.size() + 3) & ~(size_t)3, 0);
                 kbase = tabs.size();
                 tabs.resize(kbase + ((size_t)2 << a.nk), 0);
                 for (int64_t kk = 0; kk < ((int64_t)1 << a.nk); kk++) {
@@ -339,12 +408,15 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
                     tabs[kbase + 2 * kk] = ka;
                     tabs[kbase + 2 * kk + 1] = kb;
                 }
-                fixes.push_back({d->launches.size(), 1, kbase});
+                fixes.push_back({P.launches.size(), 1, kbase});
             }
             const int64_t total = a.R * p.n_orbits;
             L.team = (total < 148 * 512 && a.nk >= 4) ? 32 : 1;
             L.grid = grid_for(total * L.team, 256, 148 * 8);
             L.smem = (size_t)p.ntab * 256 * 4 * 4 + (a.nk <= kern::KTAB_MAX_BITS ? ((size_t)8 << a.nk) : 0);
+            L.a_bytes = a.a_elems * 8;
+            L.b_bytes = a.b_elems * 8;
+            L.c_bytes = a.R * a.c_row * 8;
             L.m = p.n_orbits;
             L.n = (int64_t)1 << a.n_inner;
             L.k = (int64_t)1 << a.nk;
@@ -373,13 +445,14 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
                 std::vector<int> mm(lm), kk(lk);
                 for (int t = 0; t < lm; t++) mm[g.aM.dst[t]] = g.aM.src[t];
                 for (int t = 0; t < lk; t++) kk[g.aK.dst[t]] = g.aK.src[t];
-                size_t base = tabs.size();
+                tabs.resize((tabs.size() + 3) & ~(size_t)3, 0);
+            size_t base = tabs.size();
                 std::vector<uint32_t> t1((size_t)p.ntm * 256, 0), t2((size_t)p.ntk * 256, 0);
                 if (p.ntm) push_tables(t1, mm, 1, 0);
                 if (p.ntk) push_tables(t2, kk, 1, 0);
                 tabs.insert(tabs.end(), t1.begin(), t1.end());
                 tabs.insert(tabs.end(), t2.begin(), t2.end());
-                fixes.push_back({d->launches.size(), 2, base});
+                fixes.push_back({P.launches.size(), 2, base});
                 L.smem = (size_t)(p.ntm + p.ntk) * 256 * 4;
                 L.grid = grid_for(Mp * g.k, 256, 148 * 16);
             } else if (st.kind == K_PREP_B) {
@@ -395,13 +468,14 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
                 std::vector<int> nn(ln), kk(lk);
                 for (int t = 0; t < ln; t++) nn[g.bN.dst[t]] = g.bN.src[t];
                 for (int t = 0; t < lk; t++) kk[g.bK.dst[t]] = g.bK.src[t];
-                size_t base = tabs.size();
+                tabs.resize((tabs.size() + 3) & ~(size_t)3, 0);
+            size_t base = tabs.size();
                 std::vector<uint32_t> t1((size_t)p.ntn * 256, 0), t2((size_t)p.ntk * 256, 0);
                 if (p.ntn) push_tables(t1, nn, 1, 0);
                 if (p.ntk) push_tables(t2, kk, 1, 0);
                 tabs.insert(tabs.end(), t1.begin(), t1.end());
                 tabs.insert(tabs.end(), t2.begin(), t2.end());
-                fixes.push_back({d->launches.size(), 3, base});
+                fixes.push_back({P.launches.size(), 3, base});
                 L.smem = (size_t)(p.ntn + p.ntk) * 256 * 4;
                 L.grid = grid_for(g.n * g.k, 256, 148 * 16);
             } else {
@@ -409,7 +483,7 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
                 if (!make_map(&L.tm[0], ptr(g.Ahi), Mp, K2) || !make_map(&L.tm[1], ptr(g.Alo), Mp, K2) ||
                     !make_map(&L.tm[2], ptr(g.Bhi), N2, K2) || !make_map(&L.tm[3], ptr(g.Blo), N2, K2)) {
                     err = "cuTensorMapEncodeTiled failed";
-                    return fail(TN_ECUDA);
+                    return TN_ECUDA;
                 }
                 L.gC = (float*)ptr(g.C);
                 L.gMp = Mp;
@@ -425,31 +499,128 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
             L.M = st.rp.M;
             L.grid = grid_for(st.rp.M, 256, 148 * 8);
         }
-        d->launches.push_back(L);
+        P.launches.push_back(L);
     }
     if (!tabs.empty()) {
-        CKF(cudaMalloc(&d->tables, tabs.size() * 4));
-        CKF(cudaMemcpy(d->tables, tabs.data(), tabs.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&P.tables, tabs.size() * 4));
+        CK(cudaMemcpy(P.tables, tabs.data(), tabs.size() * 4, cudaMemcpyHostToDevice));
     }
     for (const TabFix& f : fixes) {
-        Launch& L = d->launches[f.launch];
-        const uint32_t* p = d->tables + f.off;
+        Launch& L = P.launches[f.launch];
+        const uint32_t* p = P.tables + f.off;
         if (f.which == 0) L.ap.tab = p;
         else if (f.which == 1) L.ap.ktab = p;
         else if (f.which == 2) L.pa.tab = p;
         else L.pb.tab = p;
     }
 
-    // ---------------------------------------------------------------- capture the per-slice graph
-    CKF(cudaStreamBeginCapture(d->stream, cudaStreamCaptureModeThreadLocal));
-    for (const Launch& L : d->launches) do_launch(d, L, d->stream);
-    cudaError_t ce = cudaStreamEndCapture(d->stream, &d->graph);
+    P.launches = fuse_small(P, P.launches);
+    if (!P.msteps_host.empty()) {
+        CK(cudaMalloc(&P.msteps, P.msteps_host.size() * sizeof(kern::MStep)));
+        CK(cudaMemcpy(P.msteps, P.msteps_host.data(), P.msteps_host.size() * sizeof(kern::MStep),
+                      cudaMemcpyHostToDevice));
+        size_t nsync = 0;
+        for (const Launch& L : P.launches)
+            if (L.kind == K_MULTI) nsync = std::max(nsync, L.m_sync + L.m_n + 1);
+        CK(cudaMalloc(&P.sync, nsync * sizeof(int)));
+    }
+    CK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&P.done, cudaEventDisableTiming));
+    CK(cudaMalloc(&P.acc, std::max<int64_t>(d->M, 1) * sizeof(double2)));
+    CK(cudaMalloc(&P.counter, sizeof(int64_t)));
+    P.slice_cap = 1024;
+    CK(cudaMalloc(&P.slice_ids, P.slice_cap * sizeof(uint64_t)));
+    CK(cudaMemset(P.slice_ids, 0, P.slice_cap * sizeof(uint64_t)));
+    CK(cudaMemset(P.counter, 0, sizeof(int64_t)));
+    CK(cudaStreamBeginCapture(P.stream, cudaStreamCaptureModeThreadLocal));
+    for (const Launch& L : P.launches) do_launch(d, P, L, P.stream);
+    cudaError_t ce = cudaStreamEndCapture(P.stream, &P.graph);
     if (ce != cudaSuccess) {
         err = std::string("graph capture failed: ") + cudaGetErrorString(ce);
-        return fail(TN_ECUDA);
+        return TN_ECUDA;
     }
-    CKF(cudaGraphInstantiate(&d->gexec, d->graph, 0));
-    CKF(cudaStreamSynchronize(d->stream));
+    CK(cudaGraphInstantiate(&P.gexec, P.graph, 0));
+    CK(cudaStreamSynchronize(P.stream));
+    return TN_OK;
+}
+
+__global__ void k_sum_pipes(double2* const* accs, int np, float2* __restrict__ out, int64_t M) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x) {
+        double x = 0, y = 0;
+        for (int p = 0; p < np; p++) {  // fixed order over pipelines (deterministic)
+            x += accs[p][j].x;
+            y += accs[p][j].y;
+        }
+        out[j] = make_float2((float)x, (float)y);
+    }
+}
+
+}  // namespace
+
+int dev_bind(Device** out, const Program& prog, int device, void* workspace, size_t bytes, void* stream, int64_t M,
+             int max_pipes, std::string& err) {
+    *out = nullptr;
+    Device* d = new Device();
+    auto fail = [&](int code) {
+        dev_destroy(d);
+        return code;
+    };
+    d->dev = device;
+    d->M = M;
+    d->s = prog.s;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        err = "cudaSetDevice failed (no GPU?)";
+        delete d;
+        return TN_ECUDA;
+    }
+    {
+        int rc = set_smem_attrs(err);
+        if (rc) return fail(rc);
+    }
+    d->user = (cudaStream_t)stream;
+#define CKF(x)                                                                   \
+    do {                                                                         \
+        cudaError_t e_ = (x);                                                    \
+        if (e_ != cudaSuccess) {                                                 \
+            err = std::string(#x) + " failed: " + cudaGetErrorString(e_);        \
+            return fail(TN_ECUDA);                                               \
+        }                                                                        \
+    } while (0)
+    CKF(cudaEventCreate(&d->ev0));
+    CKF(cudaEventCreate(&d->ev1));
+    CKF(cudaEventCreateWithFlags(&d->evu, cudaEventDisableTiming));
+    const int64_t wb = (prog.work_bytes + 4095) & ~(int64_t)4095;
+    int np = 1;
+    if (workspace) {
+        if ((int64_t)bytes < prog.work_bytes) {
+            std::ostringstream o;
+            o << "workspace too small: need " << prog.work_bytes << " bytes, got " << bytes;
+            err = o.str();
+            return fail(TN_ENOMEM);
+        }
+        np = (int)std::max<int64_t>(1, std::min<int64_t>(max_pipes, (int64_t)bytes / wb));
+        d->work_all = (char*)workspace;
+    } else {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        np = (int)std::max<int64_t>(1, std::min<int64_t>(max_pipes, (int64_t)(fr / 2) / wb));
+        if (cudaMalloc(&d->work_all, (size_t)wb * np) != cudaSuccess) {
+            err = "cudaMalloc(workspace) failed";
+            return fail(TN_ENOMEM);
+        }
+        d->own_work = true;
+    }
+    CKF(cudaMalloc(&d->bank, std::max<size_t>(prog.bank.size() * 4, 16)));
+    CKF(cudaMemcpy(d->bank, prog.bank.data(), prog.bank.size() * 4, cudaMemcpyHostToDevice));
+    CKF(cudaMalloc(&d->maps, std::max<size_t>(prog.maps.size(), 16)));
+    if (!prog.maps.empty()) CKF(cudaMemcpy(d->maps, prog.maps.data(), prog.maps.size(), cudaMemcpyHostToDevice));
+    CKF(cudaMalloc(&d->out, std::max<int64_t>(M, 1) * sizeof(float2)));
+    d->pipes.resize(np);
+    for (int p = 0; p < np; p++) {
+        d->pipes[p].work = d->work_all + (size_t)p * wb;
+        int rc = build_pipe(d, d->pipes[p], prog, err);
+        if (rc) return fail(rc);
+    }
 #undef CKF
     *out = d;
     return TN_OK;
@@ -458,30 +629,51 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
 int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_out, bool out_dev, double* secs,
                  std::string& err) {
     CK(cudaSetDevice(d->dev));
-    if (n > d->slice_cap) {
-        CK(cudaFree(d->slice_ids));
-        d->slice_cap = std::max<int64_t>(n, 2 * d->slice_cap);
-        CK(cudaMalloc(&d->slice_ids, d->slice_cap * sizeof(uint64_t)));
-    }
+    const int np = (int)std::min<int64_t>((int64_t)d->pipes.size(), n);
     // order after the caller's pending work
     CK(cudaEventRecord(d->evu, d->user));
-    CK(cudaStreamWaitEvent(d->stream, d->evu, 0));
-    CK(cudaMemcpyAsync(d->slice_ids, ids_sorted, n * sizeof(uint64_t), cudaMemcpyHostToDevice, d->stream));
-    CK(cudaMemsetAsync(d->acc, 0, d->M * sizeof(double2), d->stream));
-    CK(cudaMemsetAsync(d->counter, 0, sizeof(int64_t), d->stream));
-    CK(cudaEventRecord(d->ev0, d->stream));
-    for (int64_t i = 0; i < n; i++) CK(cudaGraphLaunch(d->gexec, d->stream));
-    float2* dst = out_dev ? (float2*)amps_out : d->out;
-    kern::k_finalize<<<grid_for(d->M, 256, 148 * 8), 256, 0, d->stream>>>(d->acc, dst, d->M);
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(d->ev1, d->stream));
-    if (!out_dev) {
-        CK(cudaMemcpyAsync(amps_out, d->out, d->M * sizeof(float2), cudaMemcpyDeviceToHost, d->stream));
-        CK(cudaStreamSynchronize(d->stream));
-    } else {
-        CK(cudaEventRecord(d->evu, d->stream));
-        CK(cudaStreamWaitEvent(d->user, d->evu, 0));
+    CK(cudaEventRecord(d->ev0, d->user));
+    std::vector<double2*> accs;
+    for (int p = 0; p < (int)d->pipes.size(); p++) {
+        Pipe& P = d->pipes[p];
+        // contiguous block p of the ascending slice list (sizes differ by <= 1)
+        const int64_t base = n / np, extra = n % np;
+        const int64_t start = (p < np) ? p * base + std::min<int64_t>(p, extra) : n;
+        const int64_t cnt = (p < np) ? base + (p < extra ? 1 : 0) : 0;
+        if (cnt == 0) continue;
+        if (cnt > P.slice_cap) {
+            CK(cudaFree(P.slice_ids));
+            P.slice_cap = std::max<int64_t>(cnt, 2 * P.slice_cap);
+            CK(cudaMalloc(&P.slice_ids, P.slice_cap * sizeof(uint64_t)));
+        }
+        CK(cudaStreamWaitEvent(P.stream, d->evu, 0));
+        CK(cudaMemcpyAsync(P.slice_ids, ids_sorted + start, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice, P.stream));
+        CK(cudaMemsetAsync(P.acc, 0, d->M * sizeof(double2), P.stream));
+        CK(cudaMemsetAsync(P.counter, 0, sizeof(int64_t), P.stream));
+        for (int64_t i = 0; i < cnt; i++) CK(cudaGraphLaunch(P.gexec, P.stream));
+        CK(cudaEventRecord(P.done, P.stream));
+        accs.push_back(P.acc);
     }
+    Pipe& P0 = d->pipes[0];
+    for (int p = 1; p < np; p++) CK(cudaStreamWaitEvent(P0.stream, d->pipes[p].done, 0));
+    float2* dst = out_dev ? (float2*)amps_out : d->out;
+    if (accs.size() == 1) {
+        kern::k_finalize<<<grid_for(d->M, 256, 148 * 8), 256, 0, P0.stream>>>(accs[0], dst, d->M);
+    } else {
+        double2** dacc = nullptr;
+        CK(cudaMallocAsync(&dacc, accs.size() * sizeof(double2*), P0.stream));
+        CK(cudaMemcpyAsync(dacc, accs.data(), accs.size() * sizeof(double2*), cudaMemcpyHostToDevice, P0.stream));
+        k_sum_pipes<<<grid_for(d->M, 256, 148 * 8), 256, 0, P0.stream>>>(dacc, (int)accs.size(), dst, d->M);
+        CK(cudaFreeAsync(dacc, P0.stream));
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(d->ev1, P0.stream));
+    if (!out_dev) {
+        CK(cudaMemcpyAsync(amps_out, d->out, d->M * sizeof(float2), cudaMemcpyDeviceToHost, P0.stream));
+        CK(cudaStreamSynchronize(P0.stream));
+    }
+    CK(cudaEventRecord(d->evu, P0.stream));
+    CK(cudaStreamWaitEvent(d->user, d->evu, 0));
     if (secs) {
         CK(cudaEventSynchronize(d->ev1));
         float ms = 0;
@@ -494,24 +686,25 @@ int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_ou
 int dev_profile(Device* d, uint64_t slice_id, tn_launch_stat* stats, int max_stats, int* n_stats, std::string& err) {
     CK(cudaSetDevice(d->dev));
     CK(cudaStreamSynchronize(d->user));
-    CK(cudaMemcpyAsync(d->slice_ids, &slice_id, sizeof(uint64_t), cudaMemcpyHostToDevice, d->stream));
-    CK(cudaMemsetAsync(d->counter, 0, sizeof(int64_t), d->stream));
-    CK(cudaMemsetAsync(d->acc, 0, d->M * sizeof(double2), d->stream));
-    const int nl = (int)d->launches.size();
+    Pipe& P = d->pipes[0];
+    CK(cudaMemcpyAsync(P.slice_ids, &slice_id, sizeof(uint64_t), cudaMemcpyHostToDevice, P.stream));
+    CK(cudaMemsetAsync(P.counter, 0, sizeof(int64_t), P.stream));
+    CK(cudaMemsetAsync(P.acc, 0, d->M * sizeof(double2), P.stream));
+    const int nl = (int)P.launches.size();
     std::vector<cudaEvent_t> ev(nl + 1);
     for (auto& e : ev) CK(cudaEventCreate(&e));
-    CK(cudaEventRecord(ev[0], d->stream));
+    CK(cudaEventRecord(ev[0], P.stream));
     for (int i = 0; i < nl; i++) {
-        do_launch(d, d->launches[i], d->stream);
+        do_launch(d, P, P.launches[i], P.stream);
         CK(cudaGetLastError());
-        CK(cudaEventRecord(ev[i + 1], d->stream));
+        CK(cudaEventRecord(ev[i + 1], P.stream));
     }
-    CK(cudaStreamSynchronize(d->stream));
+    CK(cudaStreamSynchronize(P.stream));
     int w = 0;
     for (int i = 0; i < nl && w < max_stats; i++, w++) {
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
-        const Launch& L = d->launches[i];
+        const Launch& L = P.launches[i];
         tn_launch_stat& s = stats[w];
         s.kind = L.kind;
         s.step = L.pair;
@@ -528,24 +721,31 @@ int dev_profile(Device* d, uint64_t slice_id, tn_launch_stat* stats, int max_sta
     return TN_OK;
 }
 
+int dev_pipes(const Device* d) { return d ? (int)d->pipes.size() : 0; }
+
 void dev_destroy(Device* d) {
     if (!d) return;
     cudaSetDevice(d->dev);
-    if (d->stream) cudaStreamSynchronize(d->stream);
-    if (d->gexec) cudaGraphExecDestroy(d->gexec);
-    if (d->graph) cudaGraphDestroy(d->graph);
-    if (d->own_work && d->work) cudaFree(d->work);
+    for (Pipe& P : d->pipes) {
+        if (P.stream) cudaStreamSynchronize(P.stream);
+        if (P.gexec) cudaGraphExecDestroy(P.gexec);
+        if (P.graph) cudaGraphDestroy(P.graph);
+        cudaFree(P.tables);
+        cudaFree(P.acc);
+        cudaFree(P.counter);
+        cudaFree(P.slice_ids);
+        cudaFree(P.msteps);
+        cudaFree(P.sync);
+        if (P.done) cudaEventDestroy(P.done);
+        if (P.stream) cudaStreamDestroy(P.stream);
+    }
+    if (d->own_work && d->work_all) cudaFree(d->work_all);
     cudaFree(d->bank);
     cudaFree(d->maps);
-    cudaFree(d->tables);
-    cudaFree(d->acc);
     cudaFree(d->out);
-    cudaFree(d->slice_ids);
-    cudaFree(d->counter);
     if (d->ev0) cudaEventDestroy(d->ev0);
     if (d->ev1) cudaEventDestroy(d->ev1);
     if (d->evu) cudaEventDestroy(d->evu);
-    if (d->stream) cudaStreamDestroy(d->stream);
     delete d;
 }
 

@@ -134,6 +134,94 @@ __global__ void __launch_bounds__(256) k_apply(const ApplyDev p) {
     }
 }
 
+// ---------------------------------------------------------------------------- small-step megakernel
+// A run of consecutive small contraction steps executed by ONE persistent launch.  Work items are
+// (step, chunk of 256 orbits) in program order; a block takes the next ticket, waits until the steps
+// it depends on (RAW / WAR / WAW on workspace buffers) have all their chunks done, computes one orbit
+// per thread, and publishes its chunk.  A block only waits on tickets already taken by running blocks,
+// so the scheme cannot deadlock.  Operands are read with ld.global.cg (L2) because the workspace is
+// reused within the run.
+constexpr int MULTI_MAX_DEPS = 8;
+struct MStep {
+    const float2* A;
+    const float2* B;
+    float2* C;
+    const int32_t* ma;
+    const int32_t* mb;
+    int64_t a_row, b_row, c_row, n_orbits, total, item_begin;
+    const uint32_t* tab;
+    const uint32_t* ktab;
+    int ntab, nk, ni, ndep, chunks, pad;
+    int dep[MULTI_MAX_DEPS];
+    uint32_t inner_c[16], inner_b[16];
+};
+
+__global__ void __launch_bounds__(256) k_multi(const MStep* __restrict__ steps, int nsteps, int64_t n_items,
+                                               int* __restrict__ sync) {
+    int* ticket = sync;
+    int* done = sync + 1;
+    __shared__ int s_item, s_step;
+    while (true) {
+        if (threadIdx.x == 0) {
+            const int it = atomicAdd(ticket, 1);
+            s_item = it;
+            if (it < n_items) {
+                int s = 0;
+                while (s + 1 < nsteps && steps[s + 1].item_begin <= it) s++;
+                s_step = s;
+                const MStep& S = steps[s];
+                for (int d = 0; d < S.ndep; d++) {
+                    const int dd = S.dep[d];
+                    const int need = steps[dd].chunks;
+                    while (atomicAdd(&done[dd], 0) < need) __nanosleep(64);
+                }
+                __threadfence();
+            }
+        }
+        __syncthreads();
+        const int it = s_item;
+        if (it >= n_items) break;
+        const MStep& S = steps[s_step];
+        const int64_t w = (int64_t)(it - S.item_begin) * 256 + threadIdx.x;
+        if (w < S.total) {
+            const int64_t r = w / S.n_orbits;
+            const int64_t o = w - r * S.n_orbits;
+            uint32_t coff = 0, aoff = 0, boff = 0;
+            for (int t = 0; t < S.ntab; t++) {
+                const uint4 e = __ldg(((const uint4*)S.tab) + (t << 8) + (int)((o >> (8 * t)) & 255));
+                coff += e.x;
+                aoff += e.y;
+                boff += e.z;
+            }
+            const int64_t ra = S.ma ? (int64_t)__ldg(S.ma + r) : r;
+            const int64_t rb = S.mb ? (int64_t)__ldg(S.mb + r) : 0;
+            const float2* Ar = S.A + ra * S.a_row + aoff;
+            const float2* Br = S.B + rb * S.b_row + boff;
+            const int nout = 1 << S.ni;
+            const int64_t K = (int64_t)1 << S.nk;
+            float2 acc[16];
+#pragma unroll
+            for (int ii = 0; ii < 16; ii++) acc[ii] = make_float2(0.f, 0.f);
+            for (int64_t kk = 0; kk < K; kk++) {
+                const uint2 kab = __ldg(((const uint2*)S.ktab) + kk);
+                const float2 a = __ldcg(Ar + kab.x);
+#pragma unroll
+                for (int ii = 0; ii < 16; ii++)
+                    if (ii < nout) acc[ii] = cmac(acc[ii], a, __ldcg(Br + kab.y + S.inner_b[ii]));
+            }
+            float2* Cr = S.C + r * S.c_row + coff;
+#pragma unroll
+            for (int ii = 0; ii < 16; ii++)
+                if (ii < nout) __stcg(Cr + S.inner_c[ii], acc[ii]);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(&done[s_step], 1);
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------- GEMM pre-passes (row a3)
 // permute to K-major + 3xTF32 split: hi = cvt.rna.tf32(x), lo = x - hi
 __device__ __forceinline__ float tf32_hi(float x) {

@@ -265,6 +265,8 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             int64_t off = wa.alloc(Cn.bytes);
             Cn.buf = BufRef{REG_WORK, off};
             ap.C = Cn.buf;
+            ap.a_elems = sizeA;
+            ap.b_elems = sizeB;
             st.cmac = cmac;
             st.bytes = 8.0 * (double)(sizeA + sizeB + RC * ap.c_row) + (maRef.region ? 4.0 * RC : 0) + (mbRef.region ? 4.0 * RC : 0);
             prog.steps.push_back(st);

@@ -651,6 +651,7 @@ std::string find_plan(const Network& net, const std::vector<Leaf>& leaves, const
             for (const Node& N : pt.second.nodes)
                 if (node_size(N, S) > thr) cand = cand | N.legs;
             cand = andnot(cand & internal_bits, S);
+            if (ev.peak <= opt.max_elems) cand = andnot(internal_bits, S);
             int be = -1;
             double bt = 1e300;
             for (int e : internal) {
@@ -702,6 +703,7 @@ std::string find_plan(const Network& net, const std::vector<Leaf>& leaves, const
             for (const Node& N : t.nodes)
                 if (node_size(N, cx.sliced) > thr) cand = cand | N.legs;
             cand = andnot(cand & internal_bits, cx.sliced);
+            if (!need_peak) cand = andnot(internal_bits, cx.sliced);  // only the count is missing
             int be = -1;
             double bt = 1e300, bpeak = 1e300;
             for (int e : internal) {

@@ -124,7 +124,8 @@ enum StepKind : int32_t {
     K_PREP_B = 3,
     K_GEMM = 4,
     K_READOUT = 5,
-    K_PERMUTE = 6
+    K_PERMUTE = 6,
+    K_MULTI = 7
 };
 
 // General sparse-row pairwise contraction (SIMT path):
@@ -141,6 +142,7 @@ struct ApplyParams {
     int8_t kA[40], kB[40];    // contracted leg i at A bit kA[i], B bit kB[i]
     int n_inner = 0;          // number of B-free C bits computed per thread (<= 4)
     int8_t inner_c[4];        // their C bit positions
+    int64_t a_elems = 0, b_elems = 0;  // operand extents (complex elements), for hazard analysis
 };
 
 // Tensor-core path: TTGT with 3xTF32.
