@@ -12,11 +12,12 @@ extern "C" {
 #endif
 
 /* C[M][N] = A[M][K] * B[K][N] for complex64 row-major DEVICE buffers through the tensor-core path of
- * tn_contract (3xTF32 split pre-passes + the tcgen05 GEMM).  N >= 64 and K >= 16
+ * tn_contract (3xTF32 split pre-passes + the tcgen05 GEMM).  embed_a selects which
+ * operand gets the complex-as-real embedding (0: B, needs N >= 64; 1: A, needs N >= 128).  N and K >= 16
  * must be powers of two; M is arbitrary (ragged last tile).  Synchronises cuda_stream.  EINVAL on bad
  * shapes, ECUDA on a CUDA failure. */
 tn_status tn_debug_gemm_tf32x3(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
-                               void* cuda_stream);
+                               int32_t embed_a, void* cuda_stream);
 
 /* Size of the simplified network built by tn_build: alive tensors, all edges, internal
  * (sliceable) edges. */

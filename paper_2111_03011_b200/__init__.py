@@ -94,7 +94,7 @@ def lib():
     L.tn_last_error.restype = c.c_char_p
     L.tn_version.restype = c.c_char_p
     L.tn_debug_gemm_tf32x3.argtypes = [c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_int64, c.c_int64,
-                                       c.c_void_p]
+                                       c.c_int32, c.c_void_p]
     L.tn_debug_network.argtypes = [c.c_void_p, P(c.c_int64), P(c.c_int64), P(c.c_int64)]
     for name in ("tn_build", "tn_plan", "tn_plan_dump", "tn_bind_device", "tn_contract", "tn_profile_slice",
                  "tn_sample", "tn_debug_gemm_tf32x3", "tn_debug_network"):
@@ -205,7 +205,7 @@ class SparseState:
         return {"tensors": a.value, "edges": b.value, "internal_edges": c.value}
 
     # -------------------------------------------------------------- device
-    def bind(self, device: int = 0, workspace=None, stream=None, pipelines: int = 4):
+    def bind(self, device: int = 0, workspace=None, stream=None, pipelines: int = 8):
         """tn_bind_device.  workspace: a torch uint8 CUDA tensor (allocated here from torch's caching
         allocator when None, room for `pipelines` concurrent slice pipelines, capped by free memory);
         stream: a torch.cuda.Stream (current stream when None).  The library runs
@@ -270,7 +270,7 @@ class SparseState:
         return out, {"fraction": est[0], "F_norm": est[1], "xeb": est[2]}
 
 
-def debug_gemm(A, B):
+def debug_gemm(A, B, embed_a: int = 0):
     """C = A @ B (complex64 CUDA tensors) through the tcgen05 3xTF32 path (tn_debug_gemm_tf32x3)."""
     import torch
     M, K = A.shape
@@ -280,7 +280,7 @@ def debug_gemm(A, B):
     B = B.contiguous()
     C = torch.empty((M, N), dtype=torch.complex64, device=A.device)
     rc = lib().tn_debug_gemm_tf32x3(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
-                                   ctypes.c_void_p(C.data_ptr()), M, N, K,
+                                   ctypes.c_void_p(C.data_ptr()), M, N, K, int(embed_a),
                                    ctypes.c_void_p(torch.cuda.current_stream(A.device).cuda_stream))
     if rc != TN_OK:
         raise TnError(rc, "debug gemm failed")

@@ -297,9 +297,9 @@ tn_status tn_sample(const tn_ctx* cctx, const float* amps, const float* ideal_am
 // ---------------------------------------------------------------------------- debug entries
 
 tn_status tn_debug_gemm_tf32x3(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
-                               void* cuda_stream) {
+                               int32_t embed_a, void* cuda_stream) {
     std::string e;
-    int rc = tnb::debug_gemm(A, B, C, M, N, K, cuda_stream, e);
+    int rc = tnb::debug_gemm(A, B, C, M, N, K, embed_a, cuda_stream, e);
     return (tn_status)rc;
 }
 

@@ -16,7 +16,7 @@ int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_ou
                  std::string& err);
 int dev_profile(Device* d, uint64_t slice_id, tn_launch_stat* stats, int max_stats, int* n_stats, std::string& err);
 void dev_destroy(Device* d);
-int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K, void* stream,
+int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K, int ea, void* stream,
                std::string& err);
 
 }  // namespace tnb

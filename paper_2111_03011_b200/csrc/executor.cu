@@ -85,6 +85,7 @@ struct Launch {
     CUtensorMap tm[4];
     float* gC = nullptr;
     int64_t gMp = 0, gN2 = 0, gK2 = 0;
+    int gEA = 0;
     // instantiate / readout
     const InstLeafDesc* itab = nullptr;
     int in_leaves = 0;
@@ -187,7 +188,8 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
             kern::k_prep_b<<<L.grid, L.block, L.smem, st>>>(L.pb);
             break;
         case K_GEMM:
-            tc::k_gemm_tf32x3<<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp, L.gN2, L.gK2);
+            tc::k_gemm_tf32x3<<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp, L.gN2, L.gK2,
+                                                               L.gEA);
             break;
         case K_READOUT:
             kern::k_readout<<<L.grid, L.block, 0, st>>>(L.F, L.ridx, P.acc, L.M, P.counter);
@@ -202,7 +204,8 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
 // Fuse runs of consecutive small K_APPLY launches into K_MULTI launches (see kern::k_multi).
 std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
     auto small = [](const Launch& L) {
-        return L.kind == K_APPLY && L.ap.ktab != nullptr && L.ap.R * L.ap.n_orbits <= 65536 && L.cmac <= 4.0e6;
+        return L.kind == K_APPLY && L.ap.ktab != nullptr && L.ap.R * L.ap.n_orbits <= 65536 && L.cmac <= 4.0e6 &&
+               !L.ap.stage_b;
     };
     auto ov = [](const void* a, int64_t na, const void* b, int64_t nb) {
         const char* x = (const char*)a;
@@ -291,7 +294,7 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
         sync_off += run.size() + 1;
         M.rows = (int64_t)run.size();
         M.block = dim3(256);
-        M.grid = dim3((unsigned)std::min<int64_t>(items, 148 * 4));
+        M.grid = dim3((unsigned)std::min<int64_t>(items, 148 * 2));
         P.msteps_host.insert(P.msteps_host.end(), run.begin(), run.end());
         out.push_back(M);
         i = j;
@@ -411,9 +414,13 @@ int build_pipe(Device* d, Pipe& P, const Program& prog, std::string& err) {
                 fixes.push_back({P.launches.size(), 1, kbase});
             }
             const int64_t total = a.R * p.n_orbits;
-            L.team = (total < 148 * 512 && a.nk >= 4) ? 32 : 1;
+            // warp-per-orbit teams only when the orbits are too few to fill the GPU and k is long
+            L.team = (total < 148 * 256 && a.nk >= 6) ? 32 : 1;
             L.grid = grid_for(total * L.team, 256, 148 * 8);
             L.smem = (size_t)p.ntab * 256 * 4 * 4 + (a.nk <= kern::KTAB_MAX_BITS ? ((size_t)8 << a.nk) : 0);
+            p.stage_b = (a.nk <= kern::KTAB_MAX_BITS && a.b_row <= kern::STAGE_B_MAX &&
+                         (p.n_orbits * L.team) % 256 == 0) ? 1 : 0;
+            if (p.stage_b) L.smem += (size_t)a.b_row * 8;
             L.a_bytes = a.a_elems * 8;
             L.b_bytes = a.b_elems * 8;
             L.c_bytes = a.R * a.c_row * 8;
@@ -442,6 +449,7 @@ int build_pipe(Device* d, Pipe& P, const Program& prog, std::string& err) {
                 p.log2k = lk;
                 p.ntm = (lm + 7) / 8;
                 p.ntk = (lk + 7) / 8;
+                p.embed = g.embed_a;
                 std::vector<int> mm(lm), kk(lk);
                 for (int t = 0; t < lm; t++) mm[g.aM.dst[t]] = g.aM.src[t];
                 for (int t = 0; t < lk; t++) kk[g.aK.dst[t]] = g.aK.src[t];
@@ -465,6 +473,7 @@ int build_pipe(Device* d, Pipe& P, const Program& prog, std::string& err) {
                 p.log2k = lk;
                 p.ntn = (ln + 7) / 8;
                 p.ntk = (lk + 7) / 8;
+                p.embed = !g.embed_a;
                 std::vector<int> nn(ln), kk(lk);
                 for (int t = 0; t < ln; t++) nn[g.bN.dst[t]] = g.bN.src[t];
                 for (int t = 0; t < lk; t++) kk[g.bK.dst[t]] = g.bK.src[t];
@@ -479,17 +488,20 @@ int build_pipe(Device* d, Pipe& P, const Program& prog, std::string& err) {
                 L.smem = (size_t)(p.ntn + p.ntk) * 256 * 4;
                 L.grid = grid_for(g.n * g.k, 256, 148 * 16);
             } else {
-                const int64_t N2 = 2 * g.n, K2 = 2 * g.k;
-                if (!make_map(&L.tm[0], ptr(g.Ahi), Mp, K2) || !make_map(&L.tm[1], ptr(g.Alo), Mp, K2) ||
-                    !make_map(&L.tm[2], ptr(g.Bhi), N2, K2) || !make_map(&L.tm[3], ptr(g.Blo), N2, K2)) {
+                // D = X Y^T with X [Dm][2K], Y [Dn][2K] (see gemm_tc.cuh)
+                const int64_t K2 = 2 * g.k;
+                const int64_t Dm = g.embed_a ? 2 * Mp : Mp, Dn = g.embed_a ? g.n : 2 * g.n;
+                if (!make_map(&L.tm[0], ptr(g.Ahi), Dm, K2) || !make_map(&L.tm[1], ptr(g.Alo), Dm, K2) ||
+                    !make_map(&L.tm[2], ptr(g.Bhi), Dn, K2) || !make_map(&L.tm[3], ptr(g.Blo), Dn, K2)) {
                     err = "cuTensorMapEncodeTiled failed";
                     return TN_ECUDA;
                 }
                 L.gC = (float*)ptr(g.C);
-                L.gMp = Mp;
-                L.gN2 = N2;
+                L.gMp = Dm;
+                L.gN2 = g.embed_a ? g.n : 2 * g.n;
                 L.gK2 = K2;
-                L.grid = dim3((unsigned)((Mp + tc::BM - 1) / tc::BM), (unsigned)(N2 / tc::BN));
+                L.gEA = g.embed_a;
+                L.grid = dim3((unsigned)((Dm + tc::BM - 1) / tc::BM), (unsigned)(Dn / tc::BN));
                 L.block = dim3(tc::THREADS);
                 L.smem = tc::SMEM_BYTES;
             }
@@ -752,7 +764,7 @@ void dev_destroy(Device* d) {
 // ---------------------------------------------------------------------------- debug / unit entry
 // C[M][N] = A[M][K] B[K][N], complex64 row-major device buffers, through the tensor-core path
 // (prep A / prep B / tcgen05 GEMM).  M % 128 may be ragged; N >= 64 and K >= 16 powers of two.
-int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K, void* stream,
+int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K, int ea, void* stream,
                std::string& err) {
     if (set_smem_attrs(err)) return TN_ECUDA;
     if (N < 64 || K < 16 || (N & (N - 1)) || (K & (K - 1))) {
@@ -761,10 +773,14 @@ int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, i
     }
     cudaStream_t st = (cudaStream_t)stream;
     float *ahi, *alo, *bhi, *blo;
-    CK(cudaMalloc(&ahi, M * K * 8));
-    CK(cudaMalloc(&alo, M * K * 8));
-    CK(cudaMalloc(&bhi, N * K * 16));
-    CK(cudaMalloc(&blo, N * K * 16));
+    if (ea && N < 128) {
+        err = "debug_gemm: embedded-A mode needs N >= 128";
+        return TN_EINVAL;
+    }
+    CK(cudaMalloc(&ahi, M * K * (ea ? 16 : 8)));
+    CK(cudaMalloc(&alo, M * K * (ea ? 16 : 8)));
+    CK(cudaMalloc(&bhi, N * K * (ea ? 8 : 16)));
+    CK(cudaMalloc(&blo, N * K * (ea ? 8 : 16)));
     int lk = 0, ln = 0;
     while ((1ll << lk) < K) lk++;
     while ((1ll << ln) < N) ln++;
@@ -801,6 +817,7 @@ int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, i
     pa.tab = dtab;
     pa.ntm = 0;
     pa.ntk = (lk + 7) / 8;
+    pa.embed = ea;
     kern::k_prep_a<<<grid_for(M * K), 256, (size_t)pa.ntk * 1024, st>>>(pa);
     kern::PrepBDev pb;
     pb.B = (const float2*)B;
@@ -812,15 +829,18 @@ int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, i
     pb.tab = dtab + off_b;
     pb.ntn = (ln + 7) / 8;
     pb.ntk = (lk + 7) / 8;
+    pb.embed = !ea;
     kern::k_prep_b<<<grid_for(N * K), 256, (size_t)(pb.ntn + pb.ntk) * 1024, st>>>(pb);
     CUtensorMap tm[4];
-    if (!make_map(&tm[0], ahi, M, 2 * K) || !make_map(&tm[1], alo, M, 2 * K) || !make_map(&tm[2], bhi, 2 * N, 2 * K) ||
-        !make_map(&tm[3], blo, 2 * N, 2 * K)) {
+    const int64_t Dm = ea ? 2 * M : M, Dn = ea ? N : 2 * N;
+    if (!make_map(&tm[0], ahi, Dm, 2 * K) || !make_map(&tm[1], alo, Dm, 2 * K) || !make_map(&tm[2], bhi, Dn, 2 * K) ||
+        !make_map(&tm[3], blo, Dn, 2 * K)) {
         err = "cuTensorMapEncodeTiled failed";
         return TN_ECUDA;
     }
-    dim3 grid((unsigned)((M + tc::BM - 1) / tc::BM), (unsigned)(2 * N / tc::BN));
-    tc::k_gemm_tf32x3<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(tm[0], tm[1], tm[2], tm[3], C, M, 2 * N, 2 * K);
+    dim3 grid((unsigned)((Dm + tc::BM - 1) / tc::BM), (unsigned)(Dn / tc::BN));
+    tc::k_gemm_tf32x3<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(tm[0], tm[1], tm[2], tm[3], C, Dm, ea ? N : 2 * N,
+                                                                 2 * K, ea);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     cudaFree(ahi);

@@ -99,7 +99,7 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_tf32x3(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                   const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
-                  float* __restrict__ C, int64_t Mp, int64_t N2, int64_t K2) {
+                  float* __restrict__ C, int64_t Mp, int64_t N2, int64_t K2, int ea) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
@@ -191,12 +191,37 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (gm < Mp) {
-            float4* dst = (float4*)(C + gm * N2 + n0 + c0);
+        if (!ea) {
+            // D = C interleaved: row gm of D is row gm of C (real columns 2n, 2n+1 = re, im)
+            if (gm < Mp) {
+                float4* dst = (float4*)(C + gm * N2 + n0 + c0);
 #pragma unroll
-            for (int q = 0; q < 8; q++)
-                dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                     __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+                for (int q = 0; q < 8; q++)
+                    dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                         __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+            }
+        } else {
+            // embedded A: D row 2m = Re C[m][:], row 2m+1 = Im C[m][:] (lanes 2i, 2i+1 of this warp);
+            // exchange halves so that each lane writes 16 interleaved complex values
+            const bool odd = lane & 1;
+            float y[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const float x = __uint_as_float(odd ? v[j] : v[16 + j]);
+                y[j] = __shfl_xor_sync(0xffffffffu, x, 1);
+            }
+            const int64_t mc = gm >> 1;
+            if (gm < Mp) {  // here Mp counts D rows (= 2 x complex rows)
+                float4* dst = (float4*)(C + (mc * N2 + n0 + c0 + (odd ? 16 : 0)) * 2);
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const int j0 = 2 * q, j1 = 2 * q + 1;
+                    if (!odd)
+                        dst[q] = make_float4(__uint_as_float(v[j0]), y[j0], __uint_as_float(v[j1]), y[j1]);
+                    else
+                        dst[q] = make_float4(y[j0], __uint_as_float(v[16 + j0]), y[j1], __uint_as_float(v[16 + j1]));
+                }
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

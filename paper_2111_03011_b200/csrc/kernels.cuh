@@ -61,8 +61,10 @@ struct ApplyDev {
     int ntab, nk;
     int8_t kA[40], kB[40];
     uint32_t inner_c[16], inner_b[16];
+    int stage_b;           // 1: a 256-thread chunk lies in one output row; B's row is staged in smem
 };
 constexpr int KTAB_MAX_BITS = 12;
+constexpr int STAGE_B_MAX = 4096;  // complex elements of B per row staged in shared memory
 
 template <int NI, int TEAM>
 __global__ void __launch_bounds__(256) k_apply(const ApplyDev p) {
@@ -78,9 +80,66 @@ __global__ void __launch_bounds__(256) k_apply(const ApplyDev p) {
     __syncthreads();
     const int64_t K = (int64_t)1 << p.nk;
     const int lane = (TEAM == 1) ? 0 : (threadIdx.x & (TEAM - 1));
+    const int64_t total = p.R * p.n_orbits;
+    if (p.stage_b) {
+        // chunked loop: chunk c covers teams [c*256/TEAM, (c+1)*256/TEAM), all in one output row
+        float2* sB = (float2*)(sk + (has_ktab ? (2 << p.nk) : 0));
+        const int64_t per = 256 / TEAM;
+        const int64_t nchunks = total / per;
+        const int64_t span = (nchunks + gridDim.x - 1) / gridDim.x;  // contiguous chunks per block
+        const int64_t ch0 = blockIdx.x * span, ch1 = ch0 + span < nchunks ? ch0 + span : nchunks;
+        int64_t cached = -1;
+        for (int64_t ch = ch0; ch < ch1; ch++) {
+            const int64_t w = ch * per + threadIdx.x / TEAM;
+            const int64_t r = w / p.n_orbits;
+            const int64_t rb = p.mb ? (int64_t)p.mb[r] : 0;
+            if (rb != cached) {
+                __syncthreads();
+                const float2* src = p.B + rb * p.b_row;
+                for (int i = threadIdx.x; i < p.b_row; i += blockDim.x) sB[i] = src[i];
+                __syncthreads();
+                cached = rb;
+            }
+            const int64_t o = w - r * p.n_orbits;
+            uint32_t coff = 0, aoff = 0, boff = 0;
+            for (int t = 0; t < p.ntab; t++) {
+                const uint32_t* e = sm + ((t << 8) + (int)((o >> (8 * t)) & 255)) * 4;
+                coff += e[0];
+                aoff += e[1];
+                boff += e[2];
+            }
+            const int64_t ra = p.ma ? (int64_t)p.ma[r] : r;
+            const float2* __restrict__ Ar = p.A + ra * p.a_row + aoff;
+            const float2* Br = sB + boff;
+            float2 acc[1 << NI];
+#pragma unroll
+            for (int ii = 0; ii < (1 << NI); ii++) acc[ii] = make_float2(0.f, 0.f);
+            for (int64_t kk = lane; kk < K; kk += TEAM) {
+                const uint32_t ka = sk[2 * kk], kb = sk[2 * kk + 1];
+                const float2 a = Ar[ka];
+#pragma unroll
+                for (int ii = 0; ii < (1 << NI); ii++) acc[ii] = cmac(acc[ii], a, Br[kb + p.inner_b[ii]]);
+            }
+            if (TEAM > 1) {
+#pragma unroll
+                for (int ii = 0; ii < (1 << NI); ii++) {
+#pragma unroll
+                    for (int sh = TEAM / 2; sh >= 1; sh >>= 1) {
+                        acc[ii].x += __shfl_xor_sync(0xffffffffu, acc[ii].x, sh);
+                        acc[ii].y += __shfl_xor_sync(0xffffffffu, acc[ii].y, sh);
+                    }
+                }
+            }
+            if (lane == 0) {
+                float2* Cr = p.C + r * p.c_row + coff;
+#pragma unroll
+                for (int ii = 0; ii < (1 << NI); ii++) Cr[p.inner_c[ii]] = acc[ii];
+            }
+        }
+        return;
+    }
     const int64_t team0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
     const int64_t nteams = ((int64_t)gridDim.x * blockDim.x) / TEAM;
-    const int64_t total = p.R * p.n_orbits;
     for (int64_t w = team0; w < total; w += nteams) {
         const int64_t r = w / p.n_orbits;
         const int64_t o = w - r * p.n_orbits;
@@ -233,12 +292,13 @@ __device__ __forceinline__ float tf32_hi(float x) {
 struct PrepADev {
     const float2* A;
     const int32_t* ma;
-    float2* hi;
+    float2* hi;            // [Mp][K] float2 (plain) or [2Mp][K] float2 (embedded)
     float2* lo;
     int64_t Mp, K, a_row;
     int log2m, log2k;
     const uint32_t* tab;   // [ntm + ntk][256]: A offsets of m-index bytes, then of k-index bytes
     int ntm, ntk;
+    int embed;
 };
 
 __global__ void __launch_bounds__(256) k_prep_a(const PrepADev p) {
@@ -259,19 +319,29 @@ __global__ void __launch_bounds__(256) k_prep_a(const PrepADev p) {
         const int64_t ra = p.ma ? (int64_t)p.ma[r] : r;
         const float2 v = p.A[ra * p.a_row + off];
         const float2 h = make_float2(tf32_hi(v.x), tf32_hi(v.y));
-        p.hi[it] = h;
-        p.lo[it] = make_float2(v.x - h.x, v.y - h.y);
+        const float2 l = make_float2(v.x - h.x, v.y - h.y);
+        if (!p.embed) {
+            p.hi[it] = h;
+            p.lo[it] = l;
+        } else {  // rows 2m = (ar, -ai), 2m+1 = (ai, ar) along K
+            const int64_t i0 = (2 * mp) * p.K + kk, i1 = (2 * mp + 1) * p.K + kk;
+            p.hi[i0] = make_float2(h.x, -h.y);
+            p.lo[i0] = make_float2(l.x, -l.y);
+            p.hi[i1] = make_float2(h.y, h.x);
+            p.lo[i1] = make_float2(l.y, l.x);
+        }
     }
 }
 
 struct PrepBDev {
     const float2* B;
-    float2* hi;   // [2N][K] float2 = [2N][2K] fp32
+    float2* hi;   // [2N][K] float2 = [2N][2K] fp32 (embedded) or [N][K] float2 (plain)
     float2* lo;
     int64_t N, K;
     int log2k;
     const uint32_t* tab;  // [ntn + ntk][256]
     int ntn, ntk;
+    int embed;
 };
 
 __global__ void __launch_bounds__(256) k_prep_b(const PrepBDev p) {
@@ -289,6 +359,11 @@ __global__ void __launch_bounds__(256) k_prep_b(const PrepBDev p) {
         const float2 b = p.B[off];
         const float hr = tf32_hi(b.x), hi_ = tf32_hi(b.y);
         const float lr = b.x - hr, li = b.y - hi_;
+        if (!p.embed) {
+            p.hi[it] = make_float2(hr, hi_);
+            p.lo[it] = make_float2(lr, li);
+            continue;
+        }
         // Bt row 2nn = (br, -bi), row 2nn+1 = (bi, br) along K (complex-as-real embedding)
         p.hi[(2 * nn) * p.K + kk] = make_float2(hr, -hi_);
         p.lo[(2 * nn) * p.K + kk] = make_float2(lr, -li);

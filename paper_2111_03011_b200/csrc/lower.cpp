@@ -184,7 +184,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             int64_t fa = (int64_t)A->legs.size() - (int64_t)K.size();
             int64_t fb = (int64_t)B->legs.size() - (int64_t)K.size();
             int64_t m = RC << fa, n = (int64_t)1 << fb, k = (int64_t)1 << K.size();
-            use_gemm = (m >= 128 && n >= 64 && k >= 16);
+            use_gemm = (m >= 128 && n >= 64 && k >= 16) || (m >= 64 && n >= 128 && k >= 16);
             if (!use_gemm && per_row(*B) > per_row(*A)) std::swap(A, B);
         }
         // parent maps
@@ -304,7 +304,9 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
                 gp.bN.dst[t] = (int8_t)(gp.bN.n - 1 - t);
                 gp.bN.src[t] = (int8_t)bitpos(B->legs, fb[t]);
             }
-            const int64_t abytes = Mp * 2 * k * 4, bbytes = 2 * n * 2 * k * 4;
+            // embed the smaller operand in the complex-as-real GEMM (its rows double)
+            gp.embed_a = (Mp < n && n >= 128) || Mp < 128 ? 1 : 0;
+            const int64_t abytes = (gp.embed_a ? 2 : 1) * Mp * 2 * k * 4, bbytes = (gp.embed_a ? 1 : 2) * n * 2 * k * 4;
             gp.Ahi = BufRef{REG_WORK, wa.alloc(abytes)};
             gp.Alo = BufRef{REG_WORK, wa.alloc(abytes)};
             gp.Bhi = BufRef{REG_WORK, wa.alloc(bbytes)};
@@ -316,7 +318,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             sa.kind = K_PREP_A;
             sa.pair = (int)p;
             sa.gp = gp;
-            sa.bytes = 8.0 * Mp * k + 2.0 * abytes;
+            sa.bytes = 8.0 * Mp * k + 2.0 * abytes;  // read A once, write hi + lo
             Step sb;
             sb.kind = K_PREP_B;
             sb.pair = (int)p;

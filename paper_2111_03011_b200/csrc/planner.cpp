@@ -88,11 +88,17 @@ inline StepCost step_cost(int a, int b, int c, int u, double rA, double rB, doub
         const bool a_is_m = rowsA || (!rowsB && sA >= sB);
         const double sM = a_is_m ? sA : sB, sN = a_is_m ? sB : sA;
         const double m = sM / std::ldexp(1.0, kk), n = sN / std::ldexp(1.0, kk);
-        s.gemm = (m >= 128 && n >= 64 && kk >= 4);
+        s.gemm = ((m >= 128 && n >= 64) || (m >= 64 && n >= 128)) && kk >= 4;
     }
     if (s.gemm) {
-        const double ops_bytes = s.bytes + 8.0 * 4.0 * (sA + sB);  // pre-pass split + reread
+        // pre-passes read both operands and write hi + lo (the smaller one embedded, 2x), the GEMM reads
+        // them back
+        const double ops_bytes = s.bytes + 8.0 * (4.0 * (sA + sB) + 4.0 * std::min(sA, sB));
         s.time = std::max(s.cmac / C_TC, ops_bytes / BW) + 3 * T_LAUNCH;
+    } else if (rowsA && rowsB) {
+        // gather-contract: every output row re-reads its parents' rows (mostly from L2, ~3x HBM)
+        const double reread = 8.0 * rC * (std::ldexp(1.0, a) + std::ldexp(1.0, b));
+        s.time = std::max(std::max(s.cmac / C_SIMT, s.bytes / BW), reread / (3.0 * BW)) + T_LAUNCH;
     } else {
         s.time = std::max(s.cmac / C_SIMT, s.bytes / BW) + T_LAUNCH;
     }
