@@ -26,6 +26,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# concurrent slice pipelines use one stream each: give every stream its own hardware queue
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 from tn_inputs import configs  # noqa: E402
 
@@ -148,6 +150,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=20.0)
     ap.add_argument("--trials", type=int, default=0)
+    ap.add_argument("--pipelines", type=int, default=16)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -181,7 +184,7 @@ def main():
     t_plan = time.perf_counter() - t0
     t0 = time.perf_counter()
     stream = torch.cuda.current_stream(dev)
-    ss.bind(local, stream=stream)
+    ss.bind(local, stream=stream, pipelines=args.pipelines)
     torch.cuda.synchronize()
     t_bind = time.perf_counter() - t0
     s = info["s"]

@@ -107,6 +107,8 @@ typedef struct {
     double cmac_per_slice;       /* complex multiply-adds per slice (P:L294 T_c convention)   */
     double bytes_per_slice;      /* algorithmic HBM bytes per slice            */
     double gemm_cmac_per_slice;  /* part of cmac_per_slice on the tensor-core GEMM path       */
+    int64_t n_invariant_steps;   /* steps with no sliced edge below them: run once per        */
+    double invariant_cmac;       /* tn_contract, before the slices (their CMACs)              */
 } tn_plan_info;
 
 /* tn_plan -- P:L91 (complexity-greedy contraction order), P:L246 (slicing: fix index values so

@@ -55,7 +55,8 @@ class TnPlanInfo(ctypes.Structure):
                 ("n_tensors", ctypes.c_int64), ("n_steps", ctypes.c_int64), ("n_launches", ctypes.c_int64),
                 ("peak_elems", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
                 ("cmac_per_slice", ctypes.c_double), ("bytes_per_slice", ctypes.c_double),
-                ("gemm_cmac_per_slice", ctypes.c_double)]
+                ("gemm_cmac_per_slice", ctypes.c_double), ("n_invariant_steps", ctypes.c_int64),
+                ("invariant_cmac", ctypes.c_double)]
 
 
 class TnLaunchStat(ctypes.Structure):
@@ -193,6 +194,7 @@ class SparseState:
             "peak_elems": info.peak_elems, "workspace_bytes": info.workspace_bytes,
             "cmac_per_slice": info.cmac_per_slice, "bytes_per_slice": info.bytes_per_slice,
             "gemm_cmac_per_slice": info.gemm_cmac_per_slice,
+            "n_invariant_steps": info.n_invariant_steps, "invariant_cmac": info.invariant_cmac,
         }
         return self.info
 
@@ -209,7 +211,7 @@ class SparseState:
         """tn_bind_device.  workspace: a torch uint8 CUDA tensor (allocated here from torch's caching
         allocator when None, room for `pipelines` concurrent slice pipelines, capped by free memory);
         stream: a torch.cuda.Stream (current stream when None).  The library runs
-        floor(workspace bytes / per-pipeline workspace) slice pipelines concurrently (at most 8)."""
+        floor(workspace bytes / per-pipeline workspace) slice pipelines concurrently (at most 16)."""
         import torch
         if self.info is None:
             raise TnError(TN_EINVAL, "bind before plan")

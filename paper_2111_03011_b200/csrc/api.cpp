@@ -179,6 +179,10 @@ tn_status tn_plan(tn_ctx* ctx, const tn_slicing* slicing, int64_t max_tensor_siz
     I.cmac_per_slice = ctx->prog.cmac;
     I.bytes_per_slice = ctx->prog.bytes;
     I.gemm_cmac_per_slice = ctx->prog.gemm_cmac;
+    I.n_invariant_steps = 0;
+    for (const auto& st : ctx->prog.pre_steps)
+        if (st.kind == tnb::K_APPLY || st.kind == tnb::K_GEMM) I.n_invariant_steps++;
+    I.invariant_cmac = ctx->prog.pre_cmac;
     if (info) *info = I;
     return TN_OK;
 }
@@ -203,7 +207,7 @@ tn_status tn_bind_device(tn_ctx* ctx, int device, void* workspace, size_t bytes,
         ctx->dev = nullptr;
     }
     std::string e;
-    int rc = tnb::dev_bind(&ctx->dev, ctx->prog, device, workspace, bytes, cuda_stream, ctx->req.M, 8, e);
+    int rc = tnb::dev_bind(&ctx->dev, ctx->prog, device, workspace, bytes, cuda_stream, ctx->req.M, 16, e);
     if (rc) return fail(ctx, (tn_status)rc, e);
     return TN_OK;
 }

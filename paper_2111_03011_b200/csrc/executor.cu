@@ -129,6 +129,10 @@ struct Device {
     cudaStream_t user = nullptr;
     char* bank = nullptr;
     char* maps = nullptr;
+    char* pers = nullptr;            // slice-invariant results (written by the prologue)
+    bool has_pre = false;
+    Pipe pre;                        // prologue: slice-invariant steps, once per tn_contract
+    cudaEvent_t pre_done = nullptr;
     char* work_all = nullptr;
     bool own_work = false;
     float2* out = nullptr;
@@ -314,19 +318,20 @@ namespace {
 
 // Resolve the step program into launches for pipeline P (workspace base P.work), fuse small steps,
 // upload its tables and capture its per-slice graph.
-int build_pipe(Device* d, Pipe& P, const Program& prog, std::string& err) {
+int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& err) {
     auto ptr = [&](const BufRef& b) -> char* {
         switch (b.region) {
             case REG_WORK: return P.work + b.offset;
             case REG_BANK: return d->bank + b.offset;
             case REG_MAPS: return d->maps + b.offset;
+            case REG_PERS: return d->pers + b.offset;
             default: return nullptr;
         }
     };
     std::vector<uint32_t> tabs;  // concatenated; offsets recorded per launch (in uint32 units)
     struct TabFix { size_t launch; int which; size_t off; };
     std::vector<TabFix> fixes;
-    for (const Step& st : prog.steps) {
+    for (const Step& st : steps) {
         Launch L;
         L.kind = st.kind;
         L.pair = st.pair;
@@ -627,10 +632,17 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
     CKF(cudaMalloc(&d->maps, std::max<size_t>(prog.maps.size(), 16)));
     if (!prog.maps.empty()) CKF(cudaMemcpy(d->maps, prog.maps.data(), prog.maps.size(), cudaMemcpyHostToDevice));
     CKF(cudaMalloc(&d->out, std::max<int64_t>(M, 1) * sizeof(float2)));
+    CKF(cudaMalloc(&d->pers, std::max<int64_t>(prog.pers_bytes, 1024)));
+    CKF(cudaEventCreateWithFlags(&d->pre_done, cudaEventDisableTiming));
+    if (!prog.pre_steps.empty()) {
+        d->has_pre = true;
+        int rc = build_pipe(d, d->pre, prog.pre_steps, err);
+        if (rc) return fail(rc);
+    }
     d->pipes.resize(np);
     for (int p = 0; p < np; p++) {
         d->pipes[p].work = d->work_all + (size_t)p * wb;
-        int rc = build_pipe(d, d->pipes[p], prog, err);
+        int rc = build_pipe(d, d->pipes[p], prog.steps, err);
         if (rc) return fail(rc);
     }
 #undef CKF
@@ -645,6 +657,11 @@ int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_ou
     // order after the caller's pending work
     CK(cudaEventRecord(d->evu, d->user));
     CK(cudaEventRecord(d->ev0, d->user));
+    if (d->has_pre) {  // slice-invariant prologue, then every pipeline waits for it
+        CK(cudaStreamWaitEvent(d->pre.stream, d->evu, 0));
+        CK(cudaGraphLaunch(d->pre.gexec, d->pre.stream));
+        CK(cudaEventRecord(d->evu, d->pre.stream));
+    }
     std::vector<double2*> accs;
     for (int p = 0; p < (int)d->pipes.size(); p++) {
         Pipe& P = d->pipes[p];
@@ -698,6 +715,10 @@ int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_ou
 int dev_profile(Device* d, uint64_t slice_id, tn_launch_stat* stats, int max_stats, int* n_stats, std::string& err) {
     CK(cudaSetDevice(d->dev));
     CK(cudaStreamSynchronize(d->user));
+    if (d->has_pre) {  // the per-slice launches read the prologue's results
+        CK(cudaGraphLaunch(d->pre.gexec, d->pre.stream));
+        CK(cudaStreamSynchronize(d->pre.stream));
+    }
     Pipe& P = d->pipes[0];
     CK(cudaMemcpyAsync(P.slice_ids, &slice_id, sizeof(uint64_t), cudaMemcpyHostToDevice, P.stream));
     CK(cudaMemsetAsync(P.counter, 0, sizeof(int64_t), P.stream));
@@ -738,6 +759,7 @@ int dev_pipes(const Device* d) { return d ? (int)d->pipes.size() : 0; }
 void dev_destroy(Device* d) {
     if (!d) return;
     cudaSetDevice(d->dev);
+    if (d->has_pre) d->pipes.push_back(d->pre);  // freed with the others below
     for (Pipe& P : d->pipes) {
         if (P.stream) cudaStreamSynchronize(P.stream);
         if (P.gexec) cudaGraphExecDestroy(P.gexec);
@@ -754,7 +776,9 @@ void dev_destroy(Device* d) {
     if (d->own_work && d->work_all) cudaFree(d->work_all);
     cudaFree(d->bank);
     cudaFree(d->maps);
+    cudaFree(d->pers);
     cudaFree(d->out);
+    if (d->pre_done) cudaEventDestroy(d->pre_done);
     if (d->ev0) cudaEventDestroy(d->ev0);
     if (d->ev1) cudaEventDestroy(d->ev1);
     if (d->evu) cudaEventDestroy(d->evu);

@@ -62,7 +62,8 @@ struct LT {
     uint64_t qmask = 0;
     std::vector<uint64_t> rows;
     BufRef buf;
-    int64_t bytes = 0;               // allocation size if in the workspace
+    int64_t bytes = 0;               // allocation size if in the workspace / persistent region
+    bool variant = false;            // depends on a sliced edge (else computed once per tn_contract)
 };
 
 inline int bitpos(const std::vector<int>& legs, int e) {
@@ -94,7 +95,8 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     prog.s = s;
     std::map<int, int> slice_index;
     for (int i = 0; i < s; i++) slice_index[plan.sliced[i]] = i;
-    Alloc wa;
+    Alloc wa;  // per-slice workspace (reused between steps)
+    Alloc pa;  // persistent region for slice-invariant results (read by every slice)
     std::vector<LT> slot(leaves.size());
     std::ostringstream js;
     js.precision(17);
@@ -118,6 +120,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         std::vector<int> keep, sl;
         for (int e : L.legs) (slice_index.count(e) ? sl : keep).push_back(e);
         t.legs = keep;
+        t.variant = !sl.empty();
         if (sl.empty()) {
             t.buf = BufRef{REG_BANK, bank_off * 8};
         } else {
@@ -204,9 +207,16 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         std::vector<int> fa;
         for (int e : A->legs)
             if (!has(K, e)) fa.push_back(e);
+        // slice-invariant steps (no sliced edge below them) run once per tn_contract, before the slices
+        // (the sliced-network analogue of the paper's head-result reuse)
+        const bool var = X.variant || Y.variant;
+        Alloc& al = var ? wa : pa;
+        const int32_t reg = var ? REG_WORK : REG_PERS;
+        std::vector<Step>& out = var ? prog.steps : prog.pre_steps;
         LT Cn;
         Cn.qmask = qC;
         Cn.rows = rowsC;
+        Cn.variant = var;
         const double cmac = (double)RC * std::ldexp(1.0, (int)(fa.size() + fb.size() + K.size()));
         const int64_t sizeA = (int64_t)A->rows.size() << A->legs.size();
         const int64_t sizeB = (int64_t)B->rows.size() << B->legs.size();
@@ -262,14 +272,14 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             ap.n_inner = (int)std::min<size_t>(4, fbpos.size());
             for (int t = 0; t < ap.n_inner; t++) ap.inner_c[t] = (int8_t)fbpos[t];
             Cn.bytes = RC * ap.c_row * 8;
-            int64_t off = wa.alloc(Cn.bytes);
-            Cn.buf = BufRef{REG_WORK, off};
+            int64_t off = al.alloc(Cn.bytes);
+            Cn.buf = BufRef{reg, off};
             ap.C = Cn.buf;
             ap.a_elems = sizeA;
             ap.b_elems = sizeB;
             st.cmac = cmac;
             st.bytes = 8.0 * (double)(sizeA + sizeB + RC * ap.c_row) + (maRef.region ? 4.0 * RC : 0) + (mbRef.region ? 4.0 * RC : 0);
-            prog.steps.push_back(st);
+            out.push_back(st);
         } else {
             Cn.legs = fa;
             Cn.legs.insert(Cn.legs.end(), fb.begin(), fb.end());
@@ -307,12 +317,12 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             // embed the smaller operand in the complex-as-real GEMM (its rows double)
             gp.embed_a = (Mp < n && n >= 128) || Mp < 128 ? 1 : 0;
             const int64_t abytes = (gp.embed_a ? 2 : 1) * Mp * 2 * k * 4, bbytes = (gp.embed_a ? 1 : 2) * n * 2 * k * 4;
-            gp.Ahi = BufRef{REG_WORK, wa.alloc(abytes)};
-            gp.Alo = BufRef{REG_WORK, wa.alloc(abytes)};
-            gp.Bhi = BufRef{REG_WORK, wa.alloc(bbytes)};
-            gp.Blo = BufRef{REG_WORK, wa.alloc(bbytes)};
+            gp.Ahi = BufRef{reg, al.alloc(abytes)};
+            gp.Alo = BufRef{reg, al.alloc(abytes)};
+            gp.Bhi = BufRef{reg, al.alloc(bbytes)};
+            gp.Blo = BufRef{reg, al.alloc(bbytes)};
             Cn.bytes = Mp * n * 8;
-            Cn.buf = BufRef{REG_WORK, wa.alloc(Cn.bytes)};
+            Cn.buf = BufRef{reg, al.alloc(Cn.bytes)};
             gp.C = Cn.buf;
             Step sa;
             sa.kind = K_PREP_A;
@@ -330,22 +340,27 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             sg.gp = gp;
             sg.cmac = cmac;
             sg.bytes = 2.0 * abytes + 2.0 * bbytes + 8.0 * Mp * n;
-            prog.steps.push_back(sa);
-            prog.steps.push_back(sb);
-            prog.steps.push_back(sg);
-            wa.release(gp.Ahi.offset, abytes);
-            wa.release(gp.Alo.offset, abytes);
-            wa.release(gp.Bhi.offset, bbytes);
-            wa.release(gp.Blo.offset, bbytes);
-            prog.gemm_cmac += cmac;
+            out.push_back(sa);
+            out.push_back(sb);
+            out.push_back(sg);
+            al.release(gp.Ahi.offset, abytes);
+            al.release(gp.Alo.offset, abytes);
+            al.release(gp.Bhi.offset, bbytes);
+            al.release(gp.Blo.offset, bbytes);
+            if (var) prog.gemm_cmac += cmac;
         }
-        prog.cmac += cmac;
+        if (var) prog.cmac += cmac;
+        else prog.pre_cmac += cmac;
         prog.peak_elems = std::max<int64_t>(prog.peak_elems, RC << Cn.legs.size());
         // release operands held in the workspace
         if (X.buf.region == REG_WORK) wa.release(X.buf.offset, X.bytes);
         if (Y.buf.region == REG_WORK) wa.release(Y.buf.offset, Y.bytes);
+        // persistent results consumed by another invariant step can be recycled inside the prologue;
+        // those consumed by a per-slice step must stay valid for every slice
+        if (!var && X.buf.region == REG_PERS) pa.release(X.buf.offset, X.bytes);
+        if (!var && Y.buf.region == REG_PERS) pa.release(Y.buf.offset, Y.bytes);
         js << (p ? "," : "") << "{\"pair\":[" << i << "," << j << "],\"gemm\":" << (use_gemm ? 1 : 0)
-           << ",\"qmask\":" << qC << ",\"rows\":" << RC << ",\"m_rows\":" << A->rows.size() << ",\"n_rows\":" << B->rows.size()
+           << ",\"invariant\":" << (var ? 0 : 1) << ",\"qmask\":" << qC << ",\"rows\":" << RC << ",\"m_rows\":" << A->rows.size() << ",\"n_rows\":" << B->rows.size()
            << ",\"fa\":" << fa.size() << ",\"fb\":" << fb.size() << ",\"k\":" << K.size() << ",\"cmac\":" << cmac;
         if (RC <= 4096 && qC != 0) {
             js << ",\"row_keys\":[";
@@ -398,6 +413,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     prog.dump_json = js.str();
     prog.n_pairs = (int64_t)plan.order.size();
     prog.work_bytes = std::max<int64_t>(wa.peak, 1024);
+    prog.pers_bytes = std::max<int64_t>(pa.peak, 1024);
     for (const Step& x : prog.steps) prog.bytes += x.bytes;
     // largest leaf counts toward the peak as well
     for (const LT& t : slot) (void)t;

@@ -111,7 +111,7 @@ struct BitMap {
     int8_t dst[40];
 };
 
-enum BufRegion : int32_t { REG_NONE = 0, REG_WORK = 1, REG_BANK = 2, REG_MAPS = 3 };
+enum BufRegion : int32_t { REG_NONE = 0, REG_WORK = 1, REG_BANK = 2, REG_MAPS = 3, REG_PERS = 4 };
 struct BufRef {
     int32_t region = REG_NONE;
     int64_t offset = 0;   // bytes
@@ -196,12 +196,15 @@ struct InstLeafDesc {
 };
 
 struct Program {
-    std::vector<Step> steps;
+    std::vector<Step> steps;       // per slice
+    std::vector<Step> pre_steps;   // slice-invariant steps, once per tn_contract (outputs in REG_PERS)
+    int64_t pers_bytes = 0;
     std::vector<float> bank;       // complex64 leaf bank (interleaved)
     std::vector<uint8_t> maps;     // int32/int64 maps and tables
     int64_t work_bytes = 0;
     int64_t peak_elems = 0;
-    double cmac = 0, bytes = 0, gemm_cmac = 0;
+    double cmac = 0, bytes = 0, gemm_cmac = 0;  // per slice (slice-dependent steps)
+    double pre_cmac = 0;                          // once per tn_contract (slice-invariant steps)
     int64_t n_pairs = 0;
     // per-leaf slicing info for K_INSTANTIATE (also in `maps`)
     int s = 0;

@@ -172,11 +172,16 @@ def test_mac_count_identity(T, tmp_path):
     info = ss.plan(1 << c.log2_tmax, n_sliced=c.n_sliced)
     ss.dump(str(tmp_path / "p.json"))
     d = json.load(open(tmp_path / "p.json"))
-    tot = 0.0
+    tot = inv = 0.0
     for st in d["steps"]:
         assert st["cmac"] == st["rows"] * 2.0 ** (st["fa"] + st["fb"] + st["k"])
-        tot += st["cmac"]
+        if st["invariant"]:
+            inv += st["cmac"]
+        else:
+            tot += st["cmac"]
     assert tot == info["cmac_per_slice"]
+    assert inv == info["invariant_cmac"]
+    assert sum(st["invariant"] for st in d["steps"]) == info["n_invariant_steps"]
 
 
 def test_plan_deterministic(T, tmp_path):
