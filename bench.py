@@ -182,6 +182,13 @@ def main():
     t0 = time.perf_counter()
     info = ss.plan(1 << cfg.log2_tmax, n_sliced=cfg.n_sliced, seed=1, trials=args.trials)
     t_plan = time.perf_counter() - t0
+    if world > 1:  # every rank must contract the same sliced network: compare plan fingerprints
+        fp = torch.tensor([float(hash(tuple(info["sliced_wires"])) % (1 << 52)), info["cmac_per_slice"]],
+                          dtype=torch.float64, device=dev)
+        allfp = [torch.zeros_like(fp) for _ in range(world)]
+        dist.all_gather(allfp, fp)
+        if any(not torch.equal(allfp[0], x) for x in allfp):
+            raise RuntimeError("ranks produced different plans; refusing to sum inconsistent slices")
     t0 = time.perf_counter()
     stream = torch.cuda.current_stream(dev)
     ss.bind(local, stream=stream, pipelines=args.pipelines)

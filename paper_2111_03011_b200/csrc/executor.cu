@@ -86,6 +86,9 @@ struct Launch {
     float* gC = nullptr;
     int64_t gMp = 0, gN2 = 0, gK2 = 0;
     int gEA = 0;
+    const int4* gTiles = nullptr;
+    const int32_t* gPerm = nullptr;
+    int64_t gCm = 0, gCn = 0;
     // instantiate / readout
     const InstLeafDesc* itab = nullptr;
     int in_leaves = 0;
@@ -193,7 +196,7 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
             break;
         case K_GEMM:
             tc::k_gemm_tf32x3<<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp, L.gN2, L.gK2,
-                                                               L.gEA);
+                                                               L.gEA, L.gTiles, L.gPerm, L.gCm, L.gCn);
             break;
         case K_READOUT:
             kern::k_readout<<<L.grid, L.block, 0, st>>>(L.F, L.ridx, P.acc, L.M, P.counter);
@@ -479,6 +482,10 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 p.ntn = (ln + 7) / 8;
                 p.ntk = (lk + 7) / 8;
                 p.embed = !g.embed_a;
+                p.rowsel = g.grouped ? (const int32_t*)ptr(g.rowsel) : nullptr;
+                p.b_row = g.b_row;
+                p.log2n = ln;
+                if (g.grouped) p.N = g.NB * g.n;
                 std::vector<int> nn(ln), kk(lk);
                 for (int t = 0; t < ln; t++) nn[g.bN.dst[t]] = g.bN.src[t];
                 for (int t = 0; t < lk; t++) kk[g.bK.dst[t]] = g.bK.src[t];
@@ -491,11 +498,12 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 tabs.insert(tabs.end(), t2.begin(), t2.end());
                 fixes.push_back({P.launches.size(), 3, base});
                 L.smem = (size_t)(p.ntn + p.ntk) * 256 * 4;
-                L.grid = grid_for(g.n * g.k, 256, 148 * 16);
+                L.grid = grid_for(p.N * g.k, 256, 148 * 16);
             } else {
                 // D = X Y^T with X [Dm][2K], Y [Dn][2K] (see gemm_tc.cuh)
                 const int64_t K2 = 2 * g.k;
-                const int64_t Dm = g.embed_a ? 2 * Mp : Mp, Dn = g.embed_a ? g.n : 2 * g.n;
+                const int64_t ncols = g.grouped ? g.NB * g.n : g.n;  // complex columns of the prepped B
+                const int64_t Dm = g.embed_a ? 2 * Mp : Mp, Dn = g.embed_a ? ncols : 2 * ncols;
                 if (!make_map(&L.tm[0], ptr(g.Ahi), Dm, K2) || !make_map(&L.tm[1], ptr(g.Alo), Dm, K2) ||
                     !make_map(&L.tm[2], ptr(g.Bhi), Dn, K2) || !make_map(&L.tm[3], ptr(g.Blo), Dn, K2)) {
                     err = "cuTensorMapEncodeTiled failed";
@@ -507,6 +515,13 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 L.gK2 = K2;
                 L.gEA = g.embed_a;
                 L.grid = dim3((unsigned)((Dm + tc::BM - 1) / tc::BM), (unsigned)(Dn / tc::BN));
+                if (g.grouped) {
+                    L.gTiles = (const int4*)ptr(g.tiles);
+                    L.gPerm = (const int32_t*)ptr(g.perm);
+                    L.gCm = g.m;
+                    L.gCn = g.n;
+                    L.grid = dim3((unsigned)g.n_tiles, 1);
+                }
                 L.block = dim3(tc::THREADS);
                 L.smem = tc::SMEM_BYTES;
             }
@@ -854,6 +869,9 @@ int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, i
     pb.ntn = (ln + 7) / 8;
     pb.ntk = (lk + 7) / 8;
     pb.embed = !ea;
+    pb.rowsel = nullptr;
+    pb.b_row = 0;
+    pb.log2n = ln;
     kern::k_prep_b<<<grid_for(N * K), 256, (size_t)(pb.ntn + pb.ntk) * 1024, st>>>(pb);
     CUtensorMap tm[4];
     const int64_t Dm = ea ? 2 * M : M, Dn = ea ? N : 2 * N;
@@ -864,7 +882,7 @@ int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, i
     }
     dim3 grid((unsigned)((Dm + tc::BM - 1) / tc::BM), (unsigned)(Dn / tc::BN));
     tc::k_gemm_tf32x3<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(tm[0], tm[1], tm[2], tm[3], C, Dm, ea ? N : 2 * N,
-                                                                 2 * K, ea);
+                                                                 2 * K, ea, nullptr, nullptr, 0, 0);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     cudaFree(ahi);

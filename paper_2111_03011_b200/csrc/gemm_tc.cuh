@@ -99,7 +99,8 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_tf32x3(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                   const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
-                  float* __restrict__ C, int64_t Mp, int64_t N2, int64_t K2, int ea) {
+                  float* __restrict__ C, int64_t Mp, int64_t N2, int64_t K2, int ea,
+                  const int4* __restrict__ tiles, const int32_t* __restrict__ perm, int64_t cm, int64_t cn) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
@@ -108,8 +109,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t* tmem_slot = (uint32_t*)(accb + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM;
-    const int n0 = blockIdx.y * BN;
+    // grouped mode: the tile table gives (x0, xvalid, xbase, y0) / (yvalid, ybase, off, -)
+    int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    int xvalid = BM, xbase = 0, yvalid = BN, ybase = 0, goff = 0;
+    if (tiles) {
+        const int4 t0 = tiles[2 * blockIdx.x], t1 = tiles[2 * blockIdx.x + 1];
+        m0 = t0.x;
+        xvalid = t0.y;
+        xbase = t0.z;
+        n0 = t0.w;
+        yvalid = t1.x;
+        ybase = t1.y;
+        goff = t1.z;
+    }
     const int nkb = (int)(K2 / BK);
 
     if (threadIdx.x == 0) {
@@ -191,7 +203,48 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (!ea) {
+        if (tiles) {
+            // grouped scatter: D column -> gathered block p = goff + j / cn, fb = j % cn; C row perm[p]
+            if (!ea) {
+                const int rloc = row;  // D row = complex row (fa) of this group
+                if (rloc < xvalid) {
+                    const int64_t fa = (int64_t)(m0 - xbase) + rloc;
+#pragma unroll
+                    for (int q = 0; q < 16; q++) {
+                        const int c = c0 + 2 * q;
+                        if (c >= yvalid) break;
+                        const int64_t j = (int64_t)(n0 - ybase + c) >> 1;
+                        const int64_t pblk = goff + j / cn, fb = j % cn;
+                        const int64_t r = perm[pblk];
+                        *(float2*)(C + 2 * ((r * cm + fa) * cn + fb)) =
+                            make_float2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
+                    }
+                }
+            } else {
+                const bool odd = lane & 1;
+                float y[16];
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    const float x = __uint_as_float(odd ? v[j] : v[16 + j]);
+                    y[j] = __shfl_xor_sync(0xffffffffu, x, 1);
+                }
+                const int rloc = row & ~1;
+                if (rloc < xvalid) {
+                    const int64_t fa = ((int64_t)(m0 - xbase) + rloc) >> 1;
+#pragma unroll
+                    for (int q = 0; q < 16; q++) {
+                        const int c = c0 + (odd ? 16 : 0) + q;
+                        if (c >= yvalid) break;
+                        const int64_t j = (int64_t)(n0 - ybase + c);
+                        const int64_t pblk = goff + j / cn, fb = j % cn;
+                        const int64_t r = perm[pblk];
+                        const float re = odd ? y[q] : __uint_as_float(v[q]);
+                        const float im = odd ? __uint_as_float(v[16 + q]) : y[q];
+                        *(float2*)(C + 2 * ((r * cm + fa) * cn + fb)) = make_float2(re, im);
+                    }
+                }
+            }
+        } else if (!ea) {
             // D = C interleaved: row gm of D is row gm of C (real columns 2n, 2n+1 = re, im)
             if (gm < Mp) {
                 float4* dst = (float4*)(C + gm * N2 + n0 + c0);

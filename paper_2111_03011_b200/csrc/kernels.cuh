@@ -342,6 +342,9 @@ struct PrepBDev {
     const uint32_t* tab;  // [ntn + ntk][256]
     int ntn, ntk;
     int embed;
+    const int32_t* rowsel;  // grouped GEMM: B row of gathered block p = nn >> log2n (else null)
+    int64_t b_row;
+    int log2n;
 };
 
 __global__ void __launch_bounds__(256) k_prep_b(const PrepBDev p) {
@@ -353,10 +356,12 @@ __global__ void __launch_bounds__(256) k_prep_b(const PrepBDev p) {
     for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total; it += (int64_t)gridDim.x * blockDim.x) {
         const int64_t nn = it >> p.log2k;
         const int64_t kk = it & (p.K - 1);
+        const int64_t fbi = p.rowsel ? (nn & (((int64_t)1 << p.log2n) - 1)) : nn;
         uint32_t off = 0;
-        for (int t = 0; t < p.ntn; t++) off += sm[(t << 8) + (int)((nn >> (8 * t)) & 255)];
+        for (int t = 0; t < p.ntn; t++) off += sm[(t << 8) + (int)((fbi >> (8 * t)) & 255)];
         for (int t = 0; t < p.ntk; t++) off += sm[((p.ntn + t) << 8) + (int)((kk >> (8 * t)) & 255)];
-        const float2 b = p.B[off];
+        const int64_t rb = p.rowsel ? (int64_t)p.rowsel[nn >> p.log2n] : 0;
+        const float2 b = p.B[rb * p.b_row + off];
         const float hr = tf32_hi(b.x), hi_ = tf32_hi(b.y);
         const float lr = b.x - hr, li = b.y - hi_;
         if (!p.embed) {

@@ -180,8 +180,17 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         // roles
         bool use_gemm = false;
         LT *A = &X, *B = &Y;
+        bool grouped = false;
         if (rx && ry) {
             if (per_row(Y) > per_row(X)) std::swap(A, B);
+            // gather-contract on the tensor cores when the per-row GEMMs are big enough and many output
+            // rows share an A parent (grouped GEMM, see GemmParams::grouped)
+            const int64_t fa = (int64_t)A->legs.size() - (int64_t)K.size();
+            const int64_t fb = (int64_t)B->legs.size() - (int64_t)K.size();
+            const double cm = (double)RC * std::ldexp(1.0, (int)(fa + fb + K.size()));
+            const int64_t RA = (int64_t)A->rows.size();
+            grouped = K.size() >= 4 && fa >= 5 && cm >= 16.0 * 1024 * 1024 && RC >= 16 * RA;
+            use_gemm = grouped;
         } else {
             if (ry || (!rx && per_row(Y) > per_row(X))) std::swap(A, B);
             int64_t fa = (int64_t)A->legs.size() - (int64_t)K.size();
@@ -284,12 +293,13 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             Cn.legs = fa;
             Cn.legs.insert(Cn.legs.end(), fb.begin(), fb.end());
             const int64_t m = (int64_t)1 << fa.size(), n = (int64_t)1 << fb.size(), k = (int64_t)1 << K.size();
-            const int64_t Mp = RC * m;
+            const int64_t RA = (int64_t)A->rows.size();
+            const int64_t Mp = grouped ? RA * m : RC * m;  // rows of the prepped A
             GemmParams gp;
             gp.A = A->buf;
             gp.B = B->buf;
-            gp.ma = maRef;
-            gp.R = RC;
+            gp.ma = grouped ? BufRef() : maRef;
+            gp.R = grouped ? RA : RC;
             gp.m = m;
             gp.n = n;
             gp.k = k;
@@ -314,14 +324,58 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
                 gp.bN.dst[t] = (int8_t)(gp.bN.n - 1 - t);
                 gp.bN.src[t] = (int8_t)bitpos(B->legs, fb[t]);
             }
-            // embed the smaller operand in the complex-as-real GEMM (its rows double)
-            gp.embed_a = (Mp < n && n >= 128) || Mp < 128 ? 1 : 0;
-            const int64_t abytes = (gp.embed_a ? 2 : 1) * Mp * 2 * k * 4, bbytes = (gp.embed_a ? 1 : 2) * n * 2 * k * 4;
+            int64_t NBcols = n;  // complex columns of the prepped B
+            if (grouped) {
+                gp.grouped = 1;
+                gp.RC = RC;
+                gp.NB = RC;
+                gp.b_row = (int64_t)1 << B->legs.size();
+                NBcols = RC * n;
+                // group output rows by their A parent (stable), gathered B blocks in that order
+                std::vector<int32_t> perm(RC), rowsel(RC);
+                for (int64_t r = 0; r < RC; r++) perm[r] = (int32_t)r;
+                std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) { return ma[x] < ma[y]; });
+                for (int64_t q = 0; q < RC; q++) rowsel[q] = mb[perm[q]];
+                gp.perm = BufRef{REG_MAPS, push_blob(prog.maps, perm.data(), perm.size() * 4)};
+                gp.rowsel = BufRef{REG_MAPS, push_blob(prog.maps, rowsel.data(), rowsel.size() * 4)};
+                gp.embed_a = (RA * m < RC * n) ? 1 : 0;
+                const int xs = gp.embed_a ? 2 : 1, ys = gp.embed_a ? 1 : 2;
+                std::vector<GemmTile> tiles;
+                int64_t q = 0;
+                while (q < RC) {
+                    const int32_t a = ma[perm[q]];
+                    int64_t e = q;
+                    while (e < RC && ma[perm[e]] == a) e++;
+                    const int64_t xb = (int64_t)a * m * xs, xr = m * xs;
+                    const int64_t yb = q * n * ys, yr = (e - q) * n * ys;
+                    for (int64_t x0 = xb; x0 < xb + xr; x0 += 128)
+                        for (int64_t y0 = yb; y0 < yb + yr; y0 += 128) {
+                            GemmTile t;
+                            t.x0 = (int32_t)x0;
+                            t.xvalid = (int32_t)std::min<int64_t>(128, xb + xr - x0);
+                            t.xbase = (int32_t)xb;
+                            t.y0 = (int32_t)y0;
+                            t.yvalid = (int32_t)std::min<int64_t>(128, yb + yr - y0);
+                            t.ybase = (int32_t)yb;
+                            t.off = (int32_t)q;
+                            t.pad = 0;
+                            tiles.push_back(t);
+                        }
+                    q = e;
+                }
+                gp.n_tiles = (int64_t)tiles.size();
+                gp.tiles = BufRef{REG_MAPS, push_blob(prog.maps, tiles.data(), tiles.size() * sizeof(GemmTile))};
+            } else {
+                // embed the smaller operand in the complex-as-real GEMM (its rows double)
+                gp.embed_a = (Mp < n && n >= 128) || Mp < 128 ? 1 : 0;
+            }
+            const int64_t abytes = (gp.embed_a ? 2 : 1) * Mp * 2 * k * 4,
+                          bbytes = (gp.embed_a ? 1 : 2) * NBcols * 2 * k * 4;
             gp.Ahi = BufRef{reg, al.alloc(abytes)};
             gp.Alo = BufRef{reg, al.alloc(abytes)};
             gp.Bhi = BufRef{reg, al.alloc(bbytes)};
             gp.Blo = BufRef{reg, al.alloc(bbytes)};
-            Cn.bytes = Mp * n * 8;
+            Cn.bytes = RC * m * n * 8;
             Cn.buf = BufRef{reg, al.alloc(Cn.bytes)};
             gp.C = Cn.buf;
             Step sa;
@@ -333,13 +387,13 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             sb.kind = K_PREP_B;
             sb.pair = (int)p;
             sb.gp = gp;
-            sb.bytes = 8.0 * n * k + 2.0 * bbytes;
+            sb.bytes = 8.0 * NBcols * k + 2.0 * bbytes;
             Step sg;
             sg.kind = K_GEMM;
             sg.pair = (int)p;
             sg.gp = gp;
             sg.cmac = cmac;
-            sg.bytes = 2.0 * abytes + 2.0 * bbytes + 8.0 * Mp * n;
+            sg.bytes = 2.0 * abytes + 2.0 * bbytes + 8.0 * RC * m * n;
             out.push_back(sa);
             out.push_back(sb);
             out.push_back(sg);
@@ -360,7 +414,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         if (!var && X.buf.region == REG_PERS) pa.release(X.buf.offset, X.bytes);
         if (!var && Y.buf.region == REG_PERS) pa.release(Y.buf.offset, Y.bytes);
         js << (p ? "," : "") << "{\"pair\":[" << i << "," << j << "],\"gemm\":" << (use_gemm ? 1 : 0)
-           << ",\"invariant\":" << (var ? 0 : 1) << ",\"qmask\":" << qC << ",\"rows\":" << RC << ",\"m_rows\":" << A->rows.size() << ",\"n_rows\":" << B->rows.size()
+           << ",\"invariant\":" << (var ? 0 : 1) << ",\"grouped\":" << (grouped ? 1 : 0) << ",\"qmask\":" << qC << ",\"rows\":" << RC << ",\"m_rows\":" << A->rows.size() << ",\"n_rows\":" << B->rows.size()
            << ",\"fa\":" << fa.size() << ",\"fb\":" << fb.size() << ",\"k\":" << K.size() << ",\"cmac\":" << cmac;
         if (RC <= 4096 && qC != 0) {
             js << ",\"row_keys\":[";

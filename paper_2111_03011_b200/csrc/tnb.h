@@ -159,6 +159,21 @@ struct GemmParams {
     BitMap bN, bK;            // B index bits from (n index bit -> B bit), (k index bit -> B bit)
     int embed_a = 0;          // 1: embed A ([2Mp][2K] rows (ar,-ai),(ai,ar)), B plain [N][2K] ("EA");
                               // 0: A plain [Mp][2K], embed B ([2N][2K] rows (br,-bi),(bi,br)) ("EB")
+    // grouped mode (both operands carry rows, SURVEY a6 GATHER-CONTRACT on the tensor cores): output
+    // rows are grouped by their A parent; group a is the GEMM A_a [m x k] x [B_{mb[r]} for r in group]
+    // [k x n|G_a|].  A is prepped as-is (R = A's rows, no map), B is gathered in group order through
+    // `rowsel` (B row of gathered block p), and the epilogue scatters block p to output row perm[p].
+    int grouped = 0;
+    int64_t RC = 0;           // output rows (grouped)
+    int64_t NB = 0;           // gathered B blocks (= RC)
+    int64_t b_row = 0;
+    BufRef perm, rowsel, tiles;
+    int64_t n_tiles = 0;
+};
+
+// one output tile of the grouped tensor-core GEMM (D-row / D-col units, see GemmParams::grouped)
+struct GemmTile {
+    int32_t x0, xvalid, xbase, y0, yvalid, ybase, off, pad;
 };
 
 struct InstParams {

@@ -210,3 +210,31 @@ def test_sampler_matches_oracle_sampler(T, oracle_built):
     assert abs(est["F_norm"] - metrics.f_norm(amps, n)) < 1e-9
     p = np.abs(ideal.astype(np.complex64).astype(complex)) ** 2
     assert abs(est["xeb"] - metrics.linear_xeb(p[idx], n)) < 1e-6
+
+
+# ------------------------------------------------------------------------------ tensor-core paths in the pipeline
+
+@pytest.mark.parametrize("shape,cycles,L,tmax", [((3, 7), 14, 4096, 20), ((3, 8), 12, 4096, 20),
+                                                  ((5, 5), 12, 4096, 20)])
+def test_pipeline_with_tensor_core_and_grouped_gemms(T, oracle_built, tmp_path, shape, cycles, L, tmax):
+    """Plans whose steps go through the tcgen05 GEMM (plain and grouped gather-contract) match the oracle:
+    all slices = the unsliced amplitudes; for the small case also a ragged slice subset."""
+    import json
+    from oracle import sv
+    circ = cc.generate_circuit(cc.rect_layout(*shape), cycles, "ABCDCDAB", 77)
+    n = circ["n"]
+    openq = list(range(n - 6, n))
+    bits = bs.generate_groups(n, openq, L, 78)
+    ss = T.SparseState(circ, bits, bs.qubit_mask(n, openq))
+    info = ss.plan(1 << tmax, n_sliced=-1, seed=1, trials=8, time_budget_s=300)  # deterministic search
+    ss.dump(str(tmp_path / "p.json"))
+    d = json.load(open(tmp_path / "p.json"))
+    assert any(s.get("grouped") for s in d["steps"]) and any(s.get("gemm") and not s.get("grouped") for s in d["steps"])
+    ss.bind(0)
+    s = info["s"]
+    got = ss.contract(range(1 << s)).cpu().numpy()
+    want, _ = sv.amplitudes(circ, bits)
+    assert_amps_close(got, want)
+    if n <= 24 and s >= 2:
+        sub = [x for x in range(1 << s) if x % 3 != 1]
+        assert_amps_close(ss.contract(sub).cpu().numpy(), sv.sliced_amplitudes(circ, bits, info["sliced_wires"], sub))
