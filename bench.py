@@ -245,6 +245,7 @@ def main():
     ids_pinned = torch.tensor(block if block else [0], dtype=torch.int64).pin_memory()
     host_out = torch.empty(M, dtype=torch.complex64).pin_memory()
     e2e_ms = 0.0
+    e2e_each = []
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -260,7 +261,8 @@ def main():
             dist.all_reduce(torch.view_as_real(out), op=dist.ReduceOp.SUM)
         host_out.copy_(out, non_blocking=True)
         torch.cuda.synchronize()
-        e2e_ms += (time.perf_counter() - w0) * 1e3
+        e2e_each.append((time.perf_counter() - w0) * 1e3)
+        e2e_ms += e2e_each[-1]
     t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -319,7 +321,8 @@ def main():
             "bytes_per_slice": info["bytes_per_slice"],
             "time_to_M_amplitudes_s": ms_per_step * 1e-3,
             "e2e": {"value": nS / (e2e_ms * 1e-3), "unit": "slices/s", "ms_per_step": e2e_ms,
-                    "h2d_bytes_per_step": 8 * len(block), "d2h_bytes_per_step": 8 * M},
+                    "h2d_bytes_per_step": 8 * len(block), "d2h_bytes_per_step": 8 * M,
+                    "ms_each": [round(x, 2) for x in e2e_each]},
             "roofline": roof,
             "kernel_ms_per_slice": {k: round(v["ms"], 4) for k, v in by_kind.items()},
             "clocks": clocks,

@@ -87,6 +87,7 @@ struct Launch {
     int64_t gMp = 0, gN2 = 0, gK2 = 0;
     int gEA = 0;
     const int4* gTiles = nullptr;
+    int gNTiles = 0, gTilesN = 1;
     const int32_t* gPerm = nullptr;
     int64_t gCm = 0, gCn = 0;
     // instantiate / readout
@@ -196,7 +197,8 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
             break;
         case K_GEMM:
             tc::k_gemm_tf32x3<<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp, L.gN2, L.gK2,
-                                                               L.gEA, L.gTiles, L.gPerm, L.gCm, L.gCn);
+                                                               L.gEA, L.gTiles, L.gPerm, L.gCm, L.gCn, L.gNTiles,
+                                                               L.gTilesN);
             break;
         case K_READOUT:
             kern::k_readout<<<L.grid, L.block, 0, st>>>(L.F, L.ridx, P.acc, L.M, P.counter);
@@ -514,14 +516,18 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 L.gN2 = g.embed_a ? g.n : 2 * g.n;
                 L.gK2 = K2;
                 L.gEA = g.embed_a;
-                L.grid = dim3((unsigned)((Dm + tc::BM - 1) / tc::BM), (unsigned)(Dn / tc::BN));
+                const int tiles_m = (int)((Dm + tc::BM - 1) / tc::BM), tiles_n = (int)(Dn / tc::BN);
+                L.gNTiles = tiles_m * tiles_n;
+                // keep the larger operand's tile shared by concurrently running CTAs (read once from HBM)
+                L.gTilesN = (Dn > Dm) ? -tiles_m : tiles_n;
                 if (g.grouped) {
                     L.gTiles = (const int4*)ptr(g.tiles);
                     L.gPerm = (const int32_t*)ptr(g.perm);
                     L.gCm = g.m;
                     L.gCn = g.n;
-                    L.grid = dim3((unsigned)g.n_tiles, 1);
+                    L.gNTiles = (int)g.n_tiles;
                 }
+                L.grid = dim3((unsigned)std::min(L.gNTiles, 148));  // persistent: one CTA per SM
                 L.block = dim3(tc::THREADS);
                 L.smem = tc::SMEM_BYTES;
             }
@@ -880,9 +886,9 @@ int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, i
         err = "cuTensorMapEncodeTiled failed";
         return TN_ECUDA;
     }
-    dim3 grid((unsigned)((Dm + tc::BM - 1) / tc::BM), (unsigned)(Dn / tc::BN));
-    tc::k_gemm_tf32x3<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(tm[0], tm[1], tm[2], tm[3], C, Dm, ea ? N : 2 * N,
-                                                                 2 * K, ea, nullptr, nullptr, 0, 0);
+    const int tiles_n = (int)(Dn / tc::BN), n_tiles = (int)(((Dm + tc::BM - 1) / tc::BM) * tiles_n);
+    tc::k_gemm_tf32x3<<<std::min(n_tiles, 148), tc::THREADS, tc::SMEM_BYTES, st>>>(
+        tm[0], tm[1], tm[2], tm[3], C, Dm, ea ? N : 2 * N, 2 * K, ea, nullptr, nullptr, 0, 0, n_tiles, tiles_n);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     cudaFree(ahi);

@@ -9,13 +9,14 @@
 //   x = hi + lo, hi = cvt.rna.tf32(x), lo = x - hi;  C = Ahi Bhi + Ahi Blo + Alo Bhi  (lo*lo dropped),
 // all three products accumulated in one fp32 TMEM accumulator.
 //
-// Kernel anatomy (sm_100a): one 128x128 output tile per CTA, 128 threads.
+// Kernel anatomy (sm_100a): persistent, one CTA per SM, 192 threads, 128x128 output tiles.
 //   warp 0 / lane 0 : TMA producer (cp.async.bulk.tensor, SWIZZLE_128B) into a 3-stage smem ring,
 //                     four 128x32 fp32 tiles per stage (Ahi, Alo, Bhi, Blo), mbarrier full/empty.
 //   warp 1 / lane 0 : MMA issuer, tcgen05.mma.cta_group::1.kind::tf32 M=128 N=128 K=8, 12 per stage,
-//                     tcgen05.commit -> empty barrier; last stage commits to the accumulator barrier.
-//   warp 2          : TMEM allocation (128 columns) / deallocation.
-//   warps 0-3       : epilogue, tcgen05.ld 32x32b (lane quarter = warp id) -> registers -> global.
+//                     tcgen05.commit -> smem empty barrier; after a tile -> TMEM-full barrier.
+//   warps 2-5       : epilogue, tcgen05.ld 32x32b (TMEM lane quarter = warp % 4) -> registers -> global,
+//                     then arrive on the TMEM-empty barrier.  The accumulator is double-buffered in TMEM
+//                     (2 x 128 columns), so the epilogue of tile i overlaps the MMAs of tile i+1.
 #pragma once
 
 #include <cuda.h>
@@ -32,8 +33,8 @@ constexpr int STAGES = 3;
 constexpr int TILE_BYTES = BM * BK * 4;              // 16 KB (BM == BN)
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;          // Ahi, Alo, Bhi, Blo
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int THREADS = 128;
-constexpr int TMEM_COLS = 128;
+constexpr int THREADS = 192;
+constexpr int TMEM_COLS = 256;  // two 128-column fp32 accumulators
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -41,6 +42,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -100,28 +105,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_tf32x3(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                   const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
                   float* __restrict__ C, int64_t Mp, int64_t N2, int64_t K2, int ea,
-                  const int4* __restrict__ tiles, const int32_t* __restrict__ perm, int64_t cm, int64_t cn) {
+                  const int4* __restrict__ tiles, const int32_t* __restrict__ perm, int64_t cm, int64_t cn,
+                  int n_tiles, int tiles_n) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* accb = empty + STAGES;
-    uint32_t* tmem_slot = (uint32_t*)(accb + 1);
+    uint64_t* tfull = empty + STAGES;   // [2]
+    uint64_t* tempty = tfull + 2;       // [2]
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // grouped mode: the tile table gives (x0, xvalid, xbase, y0) / (yvalid, ybase, off, -)
-    int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-    int xvalid = BM, xbase = 0, yvalid = BN, ybase = 0, goff = 0;
-    if (tiles) {
-        const int4 t0 = tiles[2 * blockIdx.x], t1 = tiles[2 * blockIdx.x + 1];
-        m0 = t0.x;
-        xvalid = t0.y;
-        xbase = t0.z;
-        n0 = t0.w;
-        yvalid = t1.x;
-        ybase = t1.y;
-        goff = t1.z;
-    }
     const int nkb = (int)(K2 / BK);
 
     if (threadIdx.x == 0) {
@@ -129,7 +123,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(accb, 1);
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -143,138 +140,195 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0 && lane == 0) {
-        // ------------------------------------------------------------ TMA producer
-        for (int kb = 0; kb < nkb; kb++) {
-            const int s = kb % STAGES;
-            const uint32_t ph = (kb / STAGES) & 1;
-            if (kb >= STAGES) mbar_wait(&empty[s], ph ^ 1);
-            uint8_t* st = smem + s * STAGE_BYTES;
-            mbar_expect_tx(&full[s], STAGE_BYTES);
-            const int kc = kb * BK;
-            tma_load_2d(st + 0 * TILE_BYTES, &mAhi, &full[s], kc, m0);
-            tma_load_2d(st + 1 * TILE_BYTES, &mAlo, &full[s], kc, m0);
-            tma_load_2d(st + 2 * TILE_BYTES, &mBhi, &full[s], kc, n0);
-            tma_load_2d(st + 3 * TILE_BYTES, &mBlo, &full[s], kc, n0);
-        }
-    } else if (warp == 1 && lane == 0) {
-        // ------------------------------------------------------------ MMA issuer
-        const uint32_t idesc = idesc_tf32(BM, BN);
-        for (int kb = 0; kb < nkb; kb++) {
-            const int s = kb % STAGES;
-            const uint32_t ph = (kb / STAGES) & 1;
-            mbar_wait(&full[s], ph);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-#pragma unroll
-            for (int k = 0; k < BK / 8; k++) {
-                const uint32_t koff = k * 32;  // 8 tf32 = 32 B along the swizzled 128 B row
-                const uint64_t dAhi = sdesc_sw128(st + 0 * TILE_BYTES + koff);
-                const uint64_t dAlo = sdesc_sw128(st + 1 * TILE_BYTES + koff);
-                const uint64_t dBhi = sdesc_sw128(st + 2 * TILE_BYTES + koff);
-                const uint64_t dBlo = sdesc_sw128(st + 3 * TILE_BYTES + koff);
-                const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
-                mma_tf32(tmem, dAlo, dBhi, idesc, first);  // small terms first
-                mma_tf32(tmem, dAhi, dBlo, idesc, 1u);
-                mma_tf32(tmem, dAhi, dBhi, idesc, 1u);
-            }
-            mma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
-        }
-        mma_commit(accb);
-    }
-    __syncwarp();
-
-    // ---------------------------------------------------------------- epilogue (all 4 warps)
-    mbar_wait(accb, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int row = warp * 32 + lane;  // TMEM lane = tile row
-    const int64_t gm = (int64_t)m0 + row;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t v[32];
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
-              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
-              "=r"(v[30]), "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    // tile -> (m0, n0) in D-row / D-col units, plus grouped-mode extents
+    auto tile_coords = [&](int t, int& m0, int& n0, int& xvalid, int& xbase, int& yvalid, int& ybase, int& goff) {
         if (tiles) {
-            // grouped scatter: D column -> gathered block p = goff + j / cn, fb = j % cn; C row perm[p]
-            if (!ea) {
-                const int rloc = row;  // D row = complex row (fa) of this group
-                if (rloc < xvalid) {
-                    const int64_t fa = (int64_t)(m0 - xbase) + rloc;
+            const int4 t0 = tiles[2 * t], t1 = tiles[2 * t + 1];
+            m0 = t0.x;
+            xvalid = t0.y;
+            xbase = t0.z;
+            n0 = t0.w;
+            yvalid = t1.x;
+            ybase = t1.y;
+            goff = t1.z;
+        } else if (tiles_n > 0) {  // N fastest: neighbouring CTAs share the A (M-side) tile
+            m0 = (t / tiles_n) * BM;
+            n0 = (t % tiles_n) * BN;
+            xvalid = BM;
+            xbase = 0;
+            yvalid = BN;
+            ybase = 0;
+            goff = 0;
+        } else {  // tiles_n < 0 encodes M fastest over -tiles_n M-tiles: CTAs share the B tile
+            m0 = (t % (-tiles_n)) * BM;
+            n0 = (t / (-tiles_n)) * BN;
+            xvalid = BM;
+            xbase = 0;
+            yvalid = BN;
+            ybase = 0;
+            goff = 0;
+        }
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // -------------------------------------------------------- TMA producer
+            int it = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+                int m0, n0, xv, xb, yv, yb, go;
+                tile_coords(t, m0, n0, xv, xb, yv, yb, go);
+                for (int kb = 0; kb < nkb; kb++, it++) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    if (it >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t* st = smem + s * STAGE_BYTES;
+                    mbar_expect_tx(&full[s], STAGE_BYTES);
+                    const int kc = kb * BK;
+                    tma_load_2d(st + 0 * TILE_BYTES, &mAhi, &full[s], kc, m0);
+                    tma_load_2d(st + 1 * TILE_BYTES, &mAlo, &full[s], kc, m0);
+                    tma_load_2d(st + 2 * TILE_BYTES, &mBhi, &full[s], kc, n0);
+                    tma_load_2d(st + 3 * TILE_BYTES, &mBlo, &full[s], kc, n0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // -------------------------------------------------------- MMA issuer
+            const uint32_t idesc = idesc_tf32(BM, BN);
+            int it = 0, lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, lt++) {
+                const int buf = lt & 1;
+                const uint32_t tph = (lt >> 1) & 1;
+                if (lt >= 2) mbar_wait(&tempty[buf], tph ^ 1);  // epilogue drained this accumulator
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t acc = tmem + (uint32_t)(buf * BN);
+                for (int kb = 0; kb < nkb; kb++, it++) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
 #pragma unroll
-                    for (int q = 0; q < 16; q++) {
-                        const int c = c0 + 2 * q;
-                        if (c >= yvalid) break;
-                        const int64_t j = (int64_t)(n0 - ybase + c) >> 1;
-                        const int64_t pblk = goff + j / cn, fb = j % cn;
-                        const int64_t r = perm[pblk];
-                        *(float2*)(C + 2 * ((r * cm + fa) * cn + fb)) =
-                            make_float2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
+                    for (int k = 0; k < BK / 8; k++) {
+                        const uint32_t koff = k * 32;  // 8 tf32 = 32 B along the swizzled 128 B row
+                        const uint64_t dAhi = sdesc_sw128(st + 0 * TILE_BYTES + koff);
+                        const uint64_t dAlo = sdesc_sw128(st + 1 * TILE_BYTES + koff);
+                        const uint64_t dBhi = sdesc_sw128(st + 2 * TILE_BYTES + koff);
+                        const uint64_t dBlo = sdesc_sw128(st + 3 * TILE_BYTES + koff);
+                        const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
+                        mma_tf32(acc, dAlo, dBhi, idesc, first);  // small terms first
+                        mma_tf32(acc, dAhi, dBlo, idesc, 1u);
+                        mma_tf32(acc, dAhi, dBhi, idesc, 1u);
+                    }
+                    mma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+                }
+                mma_commit(&tfull[buf]);   // accumulator ready for the epilogue
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue warps 2..5
+        const int quarter = warp & 3;         // TMEM lane quarter this warp may access
+        const int row = quarter * 32 + lane;  // TMEM lane = tile row
+        int lt = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, lt++) {
+            int m0, n0, xvalid, xbase, yvalid, ybase, goff;
+            tile_coords(t, m0, n0, xvalid, xbase, yvalid, ybase, goff);
+            const int buf = lt & 1;
+            const uint32_t tph = (lt >> 1) & 1;
+            mbar_wait(&tfull[buf], tph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int64_t gm = (int64_t)m0 + row;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN + c0);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (tiles) {
+                    // grouped scatter: D column -> gathered block p = goff + j / cn, fb = j % cn; C row perm[p]
+                    if (!ea) {
+                        if (row < xvalid) {
+                            const int64_t fa = (int64_t)(m0 - xbase) + row;
+#pragma unroll
+                            for (int q = 0; q < 16; q++) {
+                                const int c = c0 + 2 * q;
+                                if (c >= yvalid) break;
+                                const int64_t j = (int64_t)(n0 - ybase + c) >> 1;
+                                const int64_t pblk = goff + j / cn, fb = j % cn;
+                                const int64_t r = perm[pblk];
+                                *(float2*)(C + 2 * ((r * cm + fa) * cn + fb)) =
+                                    make_float2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
+                            }
+                        }
+                    } else {
+                        const bool odd = lane & 1;
+                        float y[16];
+#pragma unroll
+                        for (int j = 0; j < 16; j++) {
+                            const float x = __uint_as_float(odd ? v[j] : v[16 + j]);
+                            y[j] = __shfl_xor_sync(0xffffffffu, x, 1);
+                        }
+                        const int rloc = row & ~1;
+                        if (rloc < xvalid) {
+                            const int64_t fa = ((int64_t)(m0 - xbase) + rloc) >> 1;
+#pragma unroll
+                            for (int q = 0; q < 16; q++) {
+                                const int c = c0 + (odd ? 16 : 0) + q;
+                                if (c >= yvalid) break;
+                                const int64_t j = (int64_t)(n0 - ybase + c);
+                                const int64_t pblk = goff + j / cn, fb = j % cn;
+                                const int64_t r = perm[pblk];
+                                const float re = odd ? y[q] : __uint_as_float(v[q]);
+                                const float im = odd ? __uint_as_float(v[16 + q]) : y[q];
+                                *(float2*)(C + 2 * ((r * cm + fa) * cn + fb)) = make_float2(re, im);
+                            }
+                        }
+                    }
+                } else if (!ea) {
+                    // D = C interleaved: row gm of D is row gm of C (real columns 2n, 2n+1 = re, im)
+                    if (gm < Mp) {
+                        float4* dst = (float4*)(C + gm * N2 + n0 + c0);
+#pragma unroll
+                        for (int q = 0; q < 8; q++)
+                            dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                                 __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+                    }
+                } else {
+                    // embedded A: D row 2m = Re C[m][:], row 2m+1 = Im C[m][:] (lanes 2i, 2i+1 of this warp);
+                    // exchange halves so that each lane writes 16 interleaved complex values
+                    const bool odd = lane & 1;
+                    float y[16];
+#pragma unroll
+                    for (int j = 0; j < 16; j++) {
+                        const float x = __uint_as_float(odd ? v[j] : v[16 + j]);
+                        y[j] = __shfl_xor_sync(0xffffffffu, x, 1);
+                    }
+                    const int64_t mc = gm >> 1;
+                    if (gm < Mp) {  // here Mp counts D rows (= 2 x complex rows)
+                        float4* dst = (float4*)(C + (mc * N2 + n0 + c0 + (odd ? 16 : 0)) * 2);
+#pragma unroll
+                        for (int q = 0; q < 8; q++) {
+                            const int j0 = 2 * q, j1 = 2 * q + 1;
+                            if (!odd)
+                                dst[q] = make_float4(__uint_as_float(v[j0]), y[j0], __uint_as_float(v[j1]), y[j1]);
+                            else
+                                dst[q] = make_float4(y[j0], __uint_as_float(v[16 + j0]), y[j1],
+                                                     __uint_as_float(v[16 + j1]));
+                        }
                     }
                 }
-            } else {
-                const bool odd = lane & 1;
-                float y[16];
-#pragma unroll
-                for (int j = 0; j < 16; j++) {
-                    const float x = __uint_as_float(odd ? v[j] : v[16 + j]);
-                    y[j] = __shfl_xor_sync(0xffffffffu, x, 1);
-                }
-                const int rloc = row & ~1;
-                if (rloc < xvalid) {
-                    const int64_t fa = ((int64_t)(m0 - xbase) + rloc) >> 1;
-#pragma unroll
-                    for (int q = 0; q < 16; q++) {
-                        const int c = c0 + (odd ? 16 : 0) + q;
-                        if (c >= yvalid) break;
-                        const int64_t j = (int64_t)(n0 - ybase + c);
-                        const int64_t pblk = goff + j / cn, fb = j % cn;
-                        const int64_t r = perm[pblk];
-                        const float re = odd ? y[q] : __uint_as_float(v[q]);
-                        const float im = odd ? __uint_as_float(v[16 + q]) : y[q];
-                        *(float2*)(C + 2 * ((r * cm + fa) * cn + fb)) = make_float2(re, im);
-                    }
-                }
             }
-        } else if (!ea) {
-            // D = C interleaved: row gm of D is row gm of C (real columns 2n, 2n+1 = re, im)
-            if (gm < Mp) {
-                float4* dst = (float4*)(C + gm * N2 + n0 + c0);
-#pragma unroll
-                for (int q = 0; q < 8; q++)
-                    dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                         __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-            }
-        } else {
-            // embedded A: D row 2m = Re C[m][:], row 2m+1 = Im C[m][:] (lanes 2i, 2i+1 of this warp);
-            // exchange halves so that each lane writes 16 interleaved complex values
-            const bool odd = lane & 1;
-            float y[16];
-#pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const float x = __uint_as_float(odd ? v[j] : v[16 + j]);
-                y[j] = __shfl_xor_sync(0xffffffffu, x, 1);
-            }
-            const int64_t mc = gm >> 1;
-            if (gm < Mp) {  // here Mp counts D rows (= 2 x complex rows)
-                float4* dst = (float4*)(C + (mc * N2 + n0 + c0 + (odd ? 16 : 0)) * 2);
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const int j0 = 2 * q, j1 = 2 * q + 1;
-                    if (!odd)
-                        dst[q] = make_float4(__uint_as_float(v[j0]), y[j0], __uint_as_float(v[j1]), y[j1]);
-                    else
-                        dst[q] = make_float4(y[j0], __uint_as_float(v[16 + j0]), y[j1], __uint_as_float(v[16 + j1]));
-                }
-            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
