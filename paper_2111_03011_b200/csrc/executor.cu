@@ -80,6 +80,7 @@ struct Launch {
     // per-kind parameters
     kern::ApplyDev ap;
     int ni = 0, team = 1;
+    int rows_mode = 0;  // k_apply_rows (row-staged gather-contract)
     kern::PrepADev pa;
     kern::PrepBDev pb;
     CUtensorMap tm[4];
@@ -153,6 +154,21 @@ void launch_apply(const Launch& L, cudaStream_t st) {
     kern::k_apply<NI, TEAM><<<L.grid, L.block, L.smem, st>>>(L.ap);
 }
 
+template <int NI>
+void launch_apply_rows(const Launch& L, cudaStream_t st) {
+    kern::k_apply_rows<NI><<<L.grid, L.block, L.smem, st>>>(L.ap);
+}
+
+void launch_apply_rows_ni(const Launch& L, cudaStream_t st) {
+    switch (L.ni) {
+        case 0: launch_apply_rows<0>(L, st); break;
+        case 1: launch_apply_rows<1>(L, st); break;
+        case 2: launch_apply_rows<2>(L, st); break;
+        case 3: launch_apply_rows<3>(L, st); break;
+        default: launch_apply_rows<4>(L, st); break;
+    }
+}
+
 template <int TEAM>
 void launch_apply_ni(const Launch& L, cudaStream_t st) {
     switch (L.ni) {
@@ -172,6 +188,9 @@ int set_smem_attrs(std::string& err) {
     SETA(0, 1); SETA(1, 1); SETA(2, 1); SETA(3, 1); SETA(4, 1);
     SETA(0, 32); SETA(1, 32); SETA(2, 32); SETA(3, 32); SETA(4, 32);
 #undef SETA
+#define SETR(NI) CK(cudaFuncSetAttribute(kern::k_apply_rows<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, big))
+    SETR(0); SETR(1); SETR(2); SETR(3); SETR(4);
+#undef SETR
     CK(cudaFuncSetAttribute(kern::k_prep_a, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     CK(cudaFuncSetAttribute(kern::k_prep_b, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES));
@@ -186,7 +205,8 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
                                                             P.work, P.slice_ids, P.counter, d->s);
             break;
         case K_APPLY:
-            if (L.team == 32) launch_apply_ni<32>(L, st);
+            if (L.rows_mode) launch_apply_rows_ni(L, st);
+            else if (L.team == 32) launch_apply_ni<32>(L, st);
             else launch_apply_ni<1>(L, st);
             break;
         case K_PREP_A:
@@ -214,7 +234,7 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
 std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
     auto small = [](const Launch& L) {
         return L.kind == K_APPLY && L.ap.ktab != nullptr && L.ap.R * L.ap.n_orbits <= 65536 && L.cmac <= 4.0e6 &&
-               !L.ap.stage_b;
+               !L.ap.stage_b && !L.rows_mode;
     };
     auto ov = [](const void* a, int64_t na, const void* b, int64_t nb) {
         const char* x = (const char*)a;
@@ -425,12 +445,28 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
             }
             const int64_t total = a.R * p.n_orbits;
             // warp-per-orbit teams only when the orbits are too few to fill the GPU and k is long
-            L.team = (total < 148 * 256 && a.nk >= 6) ? 32 : 1;
+            // lanes walk k only when k is A's fastest-varying index (coalesced); else one orbit per thread
+            bool k_low = false;
+            for (int t = 0; t < a.nk; t++)
+                if (a.kA[t] == 0) k_low = true;
+            L.team = (total < 148 * 256 && a.nk >= 6 && k_low) ? 32 : 1;
             L.grid = grid_for(total * L.team, 256, 148 * 8);
             L.smem = (size_t)p.ntab * 256 * 4 * 4 + (a.nk <= kern::KTAB_MAX_BITS ? ((size_t)8 << a.nk) : 0);
             p.stage_b = (a.nk <= kern::KTAB_MAX_BITS && a.b_row <= kern::STAGE_B_MAX &&
                          (p.n_orbits * L.team) % 256 == 0) ? 1 : 0;
             if (p.stage_b) L.smem += (size_t)a.b_row * 8;
+            // gather-contract with small parent rows: one block per output row, rows staged in smem
+            if (a.nk <= kern::KTAB_MAX_BITS && (a.ma.region != REG_NONE || a.mb.region != REG_NONE) &&
+                a.a_row + a.b_row <= 12288 && a.R >= 128) {
+                L.rows_mode = 1;
+                p.stage_b = 0;
+                int kp = 1;
+                while (kp < 32 && p.n_orbits * kp * 2 <= 256 && (kp * 2) <= (1 << a.nk)) kp *= 2;
+                p.kparts = kp;
+                L.team = 1;
+                L.smem = (size_t)p.ntab * 256 * 4 * 4 + ((size_t)8 << a.nk) + (size_t)(a.a_row + a.b_row) * 8;
+                L.grid = dim3((unsigned)std::min<int64_t>(a.R, 148 * 8));
+            }
             L.a_bytes = a.a_elems * 8;
             L.b_bytes = a.b_elems * 8;
             L.c_bytes = a.R * a.c_row * 8;

@@ -62,6 +62,7 @@ struct ApplyDev {
     int8_t kA[40], kB[40];
     uint32_t inner_c[16], inner_b[16];
     int stage_b;           // 1: a 256-thread chunk lies in one output row; B's row is staged in smem
+    int kparts;            // k_apply_rows: lanes sharing one orbit (power of two <= 32)
 };
 constexpr int KTAB_MAX_BITS = 12;
 constexpr int STAGE_B_MAX = 4096;  // complex elements of B per row staged in shared memory
@@ -189,6 +190,69 @@ __global__ void __launch_bounds__(256) k_apply(const ApplyDev p) {
             float2* Cr = p.C + r * p.c_row + coff;
 #pragma unroll
             for (int ii = 0; ii < (1 << NI); ii++) Cr[p.inner_c[ii]] = acc[ii];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- row-staged gather-contract
+// (row a6, GATHER-CONTRACT with small rows) one block per output row r: both parent rows A[ma[r]] and
+// B[mb[r]] are copied to shared memory with coalesced loads, then every output of the row is computed from
+// shared memory (any bit layout); `kparts` lanes split k for one orbit and reduce with shuffles.
+template <int NI>
+__global__ void __launch_bounds__(256) k_apply_rows(const ApplyDev p) {
+    extern __shared__ uint32_t sm[];
+    const int tabn = p.ntab * 256 * 4;
+    for (int i = threadIdx.x; i < tabn; i += blockDim.x) sm[i] = p.tab[i];
+    uint32_t* sk = sm + tabn;
+    const int kn = 2 << p.nk;
+    for (int i = threadIdx.x; i < kn; i += blockDim.x) sk[i] = p.ktab[i];
+    float2* sA = (float2*)(sk + kn);
+    float2* sB = sA + p.a_row;
+    const int64_t K = (int64_t)1 << p.nk;
+    const int kparts = p.kparts;
+    const int64_t total_w = p.n_orbits * kparts;
+    for (int64_t r = blockIdx.x; r < p.R; r += gridDim.x) {
+        __syncthreads();
+        const float2* Ag = p.A + (p.ma ? (int64_t)p.ma[r] : r) * p.a_row;
+        const float2* Bg = p.B + (p.mb ? (int64_t)p.mb[r] : 0) * p.b_row;
+        for (int64_t i = threadIdx.x; i < p.a_row; i += blockDim.x) sA[i] = Ag[i];
+        for (int64_t i = threadIdx.x; i < p.b_row; i += blockDim.x) sB[i] = Bg[i];
+        __syncthreads();
+        float2* Cr = p.C + r * p.c_row;
+        for (int64_t base = 0; base < total_w; base += blockDim.x) {
+            const int64_t w = base + threadIdx.x;
+            const bool valid = w < total_w;
+            const int64_t o = valid ? w / kparts : 0;
+            const int kp = (int)(w % kparts);
+            uint32_t coff = 0, aoff = 0, boff = 0;
+            for (int t = 0; t < p.ntab; t++) {
+                const uint32_t* e = sm + ((t << 8) + (int)((o >> (8 * t)) & 255)) * 4;
+                coff += e[0];
+                aoff += e[1];
+                boff += e[2];
+            }
+            float2 acc[1 << NI];
+#pragma unroll
+            for (int ii = 0; ii < (1 << NI); ii++) acc[ii] = make_float2(0.f, 0.f);
+            if (valid) {
+                for (int64_t kk = kp; kk < K; kk += kparts) {
+                    const float2 a = sA[aoff + sk[2 * kk]];
+                    const uint32_t kb = boff + sk[2 * kk + 1];
+#pragma unroll
+                    for (int ii = 0; ii < (1 << NI); ii++) acc[ii] = cmac(acc[ii], a, sB[kb + p.inner_b[ii]]);
+                }
+            }
+            for (int sh = kparts >> 1; sh >= 1; sh >>= 1) {
+#pragma unroll
+                for (int ii = 0; ii < (1 << NI); ii++) {
+                    acc[ii].x += __shfl_xor_sync(0xffffffffu, acc[ii].x, sh);
+                    acc[ii].y += __shfl_xor_sync(0xffffffffu, acc[ii].y, sh);
+                }
+            }
+            if (valid && kp == 0) {
+#pragma unroll
+                for (int ii = 0; ii < (1 << NI); ii++) Cr[coff + p.inner_c[ii]] = acc[ii];
+            }
         }
     }
 }

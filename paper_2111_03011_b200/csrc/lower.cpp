@@ -189,7 +189,8 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             const int64_t fb = (int64_t)B->legs.size() - (int64_t)K.size();
             const double cm = (double)RC * std::ldexp(1.0, (int)(fa + fb + K.size()));
             const int64_t RA = (int64_t)A->rows.size();
-            grouped = K.size() >= 4 && fa >= 5 && cm >= 16.0 * 1024 * 1024 && RC >= 16 * RA;
+            grouped = K.size() >= 4 && fa >= 5 && cm >= 16.0 * 1024 * 1024 &&
+                      (RC >= 16 * RA || (fa >= 10 && RC >= 2 * RA));
             use_gemm = grouped;
         } else {
             if (ry || (!rx && per_row(Y) > per_row(X))) std::swap(A, B);
@@ -219,6 +220,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         // slice-invariant steps (no sliced edge below them) run once per tn_contract, before the slices
         // (the sliced-network analogue of the paper's head-result reuse)
         const bool var = X.variant || Y.variant;
+        std::string apply_json;
         Alloc& al = var ? wa : pa;
         const int32_t reg = var ? REG_WORK : REG_PERS;
         std::vector<Step>& out = var ? prog.steps : prog.pre_steps;
@@ -288,6 +290,21 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             ap.b_elems = sizeB;
             st.cmac = cmac;
             st.bytes = 8.0 * (double)(sizeA + sizeB + RC * ap.c_row) + (maRef.region ? 4.0 * RC : 0) + (mbRef.region ? 4.0 * RC : 0);
+            {
+                std::ostringstream o;
+                o << ",\"apply\":{\"dA\":" << ap.dA << ",\"dB\":" << ap.dB << ",\"dC\":" << ap.dC << ",\"kA\":[";
+                for (int t = 0; t < ap.nk; t++) o << (t ? "," : "") << (int)ap.kA[t];
+                o << "],\"kB\":[";
+                for (int t = 0; t < ap.nk; t++) o << (t ? "," : "") << (int)ap.kB[t];
+                o << "],\"cA\":[";
+                for (int t = 0; t < ap.cA.n; t++) o << (t ? "," : "") << "[" << (int)ap.cA.dst[t] << "," << (int)ap.cA.src[t] << "]";
+                o << "],\"cB\":[";
+                for (int t = 0; t < ap.cB.n; t++) o << (t ? "," : "") << "[" << (int)ap.cB.dst[t] << "," << (int)ap.cB.src[t] << "]";
+                o << "],\"inner\":[";
+                for (int t = 0; t < ap.n_inner; t++) o << (t ? "," : "") << (int)ap.inner_c[t];
+                o << "],\"ma\":" << (maRef.region ? 1 : 0) << ",\"mb\":" << (mbRef.region ? 1 : 0) << "}";
+                apply_json = o.str();
+            }
             out.push_back(st);
         } else {
             Cn.legs = fa;
@@ -415,7 +432,8 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         if (!var && Y.buf.region == REG_PERS) pa.release(Y.buf.offset, Y.bytes);
         js << (p ? "," : "") << "{\"pair\":[" << i << "," << j << "],\"gemm\":" << (use_gemm ? 1 : 0)
            << ",\"invariant\":" << (var ? 0 : 1) << ",\"grouped\":" << (grouped ? 1 : 0) << ",\"qmask\":" << qC << ",\"rows\":" << RC << ",\"m_rows\":" << A->rows.size() << ",\"n_rows\":" << B->rows.size()
-           << ",\"fa\":" << fa.size() << ",\"fb\":" << fb.size() << ",\"k\":" << K.size() << ",\"cmac\":" << cmac;
+           << ",\"fa\":" << fa.size() << ",\"fb\":" << fb.size() << ",\"k\":" << K.size() << ",\"cmac\":" << cmac
+           << apply_json;
         if (RC <= 4096 && qC != 0) {
             js << ",\"row_keys\":[";
             for (int64_t r = 0; r < RC; r++) js << (r ? "," : "") << rowsC[r];
