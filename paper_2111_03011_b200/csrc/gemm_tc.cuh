@@ -34,7 +34,9 @@ constexpr int TILE_BYTES = BM * BK * 4;              // 16 KB (BM == BN)
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;          // Ahi, Alo, Bhi, Blo
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int THREADS = 192;
-constexpr int TMEM_COLS = 256;  // two 128-column fp32 accumulators
+constexpr int KSPLIT = 2;       // k-blocks alternate between KSPLIT accumulators (summed in fp32 RN):
+                                // the tensor-core accumulator truncates, so shorter chains = less bias
+constexpr int TMEM_COLS = 512;  // 2 tile buffers x KSPLIT x 128 fp32 columns
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -201,8 +203,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const uint32_t tph = (lt >> 1) & 1;
                 if (lt >= 2) mbar_wait(&tempty[buf], tph ^ 1);  // epilogue drained this accumulator
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t acc = tmem + (uint32_t)(buf * BN);
+                const uint32_t acc0 = tmem + (uint32_t)(buf * BN * KSPLIT);
                 for (int kb = 0; kb < nkb; kb++, it++) {
+                    const uint32_t acc = acc0 + (uint32_t)((kb % KSPLIT) * BN);
                     const int s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(&full[s], ph);
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         const uint64_t dAlo = sdesc_sw128(st + 1 * TILE_BYTES + koff);
                         const uint64_t dBhi = sdesc_sw128(st + 2 * TILE_BYTES + koff);
                         const uint64_t dBlo = sdesc_sw128(st + 3 * TILE_BYTES + koff);
-                        const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
+                        const uint32_t first = (kb < KSPLIT && k == 0) ? 0u : 1u;
                         mma_tf32(acc, dAlo, dBhi, idesc, first);  // small terms first
                         mma_tf32(acc, dAhi, dBlo, idesc, 1u);
                         mma_tf32(acc, dAhi, dBhi, idesc, 1u);
@@ -241,17 +244,31 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 uint32_t v[32];
-                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN + c0);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                {
+                    float f[32];
+#pragma unroll
+                    for (int q = 0; q < 32; q++) f[q] = 0.f;
+                    const int nsplit = nkb < KSPLIT ? nkb : KSPLIT;
+                    for (int sp = 0; sp < nsplit; sp++) {
+                        uint32_t u[32];
+                        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) +
+                                               (uint32_t)((buf * KSPLIT + sp) * BN + c0);
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+                            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                            : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
+                              "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
+                              "=r"(u[14]), "=r"(u[15]), "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]),
+                              "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]),
+                              "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+                            : "r"(taddr));
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                        for (int q = 0; q < 32; q++) f[q] += __uint_as_float(u[q]);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 32; q++) v[q] = __float_as_uint(f[q]);
+                }
                 if (tiles) {
                     // grouped scatter: D column -> gathered block p = goff + j / cn, fb = j % cn; C row perm[p]
                     if (!ea) {

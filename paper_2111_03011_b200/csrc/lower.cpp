@@ -220,7 +220,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         // slice-invariant steps (no sliced edge below them) run once per tn_contract, before the slices
         // (the sliced-network analogue of the paper's head-result reuse)
         const bool var = X.variant || Y.variant;
-        std::string apply_json;
+        std::string apply_json, gemm_json;
         Alloc& al = var ? wa : pa;
         const int32_t reg = var ? REG_WORK : REG_PERS;
         std::vector<Step>& out = var ? prog.steps : prog.pre_steps;
@@ -328,6 +328,16 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
                 gp.aM.dst[t] = (int8_t)(gp.aM.n - 1 - t);             // m-index bit
                 gp.aM.src[t] = (int8_t)bitpos(A->legs, fa[t]);        // A bit
             }
+            // can an operand be TMA-loaded raw (split to hi/lo inside the GEMM)?  Its contracted legs must
+            // be its lowest bits and its rows contiguous (no row map).
+            auto low_is_K = [&](const LT* T) {
+                for (int e : K)
+                    if (bitpos(T->legs, e) >= (int)K.size()) return false;
+                return true;
+            };
+            const bool a_low = low_is_K(A) && (grouped || !maRef.region);
+            const bool b_low = low_is_K(B);
+            gemm_json = std::string(",\"a_lowK\":") + (a_low ? "1" : "0") + ",\"b_lowK\":" + (b_low ? "1" : "0");
             gp.aK.n = (int)K.size();
             gp.bK.n = (int)K.size();
             for (int t = 0; t < gp.aK.n; t++) {
@@ -433,7 +443,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         js << (p ? "," : "") << "{\"pair\":[" << i << "," << j << "],\"gemm\":" << (use_gemm ? 1 : 0)
            << ",\"invariant\":" << (var ? 0 : 1) << ",\"grouped\":" << (grouped ? 1 : 0) << ",\"qmask\":" << qC << ",\"rows\":" << RC << ",\"m_rows\":" << A->rows.size() << ",\"n_rows\":" << B->rows.size()
            << ",\"fa\":" << fa.size() << ",\"fb\":" << fb.size() << ",\"k\":" << K.size() << ",\"cmac\":" << cmac
-           << apply_json;
+           << apply_json << gemm_json;
         if (RC <= 4096 && qC != 0) {
             js << ",\"row_keys\":[";
             for (int64_t r = 0; r < RC; r++) js << (r ? "," : "") << rowsC[r];

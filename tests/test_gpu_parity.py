@@ -238,3 +238,32 @@ def test_pipeline_with_tensor_core_and_grouped_gemms(T, oracle_built, tmp_path, 
     if n <= 24 and s >= 2:
         sub = [x for x in range(1 << s) if x % 3 != 1]
         assert_amps_close(ss.contract(sub).cpu().numpy(), sv.sliced_amplitudes(circ, bits, info["sliced_wires"], sub))
+
+
+# ------------------------------------------------------------------------------ full size, bench configuration
+
+@pytest.mark.slow
+def test_config3_full_size_bench_configuration(T, oracle_built):
+    """Config 3 at BASELINE size (30 qubits, m=12, M=65536, 2^8 slices) in the launch configuration bench.py
+    times (same plan parameters, 16 concurrent slice pipelines): all slices vs the oracle's exact amplitudes
+    (one fp64 state-vector run of 2^30 amplitudes on the host), and the prefix S = [0, 2^7) (Pi_0 on w_0)."""
+    import os
+    from oracle import sv
+    c = configs.get(3)
+    circ = c.circuit()
+    n = circ["n"]
+    bits = c.bitstrings(n)
+    ss = T.SparseState(circ, bits, c.open_mask(n))
+    info = ss.plan(1 << c.log2_tmax, n_sliced=c.n_sliced, seed=1)
+    ss.bind(0, pipelines=16)
+    s = info["s"]
+    got = ss.contract(range(1 << s)).cpu().numpy()
+    threads = os.cpu_count() or 1
+    want, norm2 = sv.amplitudes(circ, bits, threads=threads)
+    assert abs(norm2 - 1) < 1e-9
+    e, worst = assert_amps_close(got, want)
+    print(f"config 3 all slices: rel L2 {e:.2e}, max |a-o|/rms {worst:.2e}")
+    got1 = ss.contract(range(1 << (s - 1))).cpu().numpy()
+    want1, _ = sv.prefix_amplitudes(circ, bits, info["sliced_wires"], 1, threads=threads)
+    e1, _ = assert_amps_close(got1, want1)
+    print(f"config 3 prefix half: rel L2 {e1:.2e}")
