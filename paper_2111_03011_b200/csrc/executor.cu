@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 #include <string>
@@ -323,7 +324,8 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
         sync_off += run.size() + 1;
         M.rows = (int64_t)run.size();
         M.block = dim3(256);
-        M.grid = dim3((unsigned)std::min<int64_t>(items, 148 * 2));
+        static const int multi_grid = getenv("TNB_MULTI_GRID") ? atoi(getenv("TNB_MULTI_GRID")) : 296;
+        M.grid = dim3((unsigned)std::min<int64_t>(items, multi_grid));
         P.msteps_host.insert(P.msteps_host.end(), run.begin(), run.end());
         out.push_back(M);
         i = j;
