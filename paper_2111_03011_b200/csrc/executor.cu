@@ -5,6 +5,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
@@ -709,8 +711,15 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
     return TN_OK;
 }
 
+static double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_out, bool out_dev, double* secs,
                  std::string& err) {
+    static const bool trace = getenv("TNB_TRACE") != nullptr;
+    const double t0 = trace ? now_ms() : 0;
+    double tA = 0, tB = 0, tC = 0;
     CK(cudaSetDevice(d->dev));
     const int np = (int)std::min<int64_t>((int64_t)d->pipes.size(), n);
     // order after the caller's pending work
@@ -742,6 +751,7 @@ int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_ou
         CK(cudaEventRecord(P.done, P.stream));
         accs.push_back(P.acc);
     }
+    if (trace) tA = now_ms();
     Pipe& P0 = d->pipes[0];
     for (int p = 1; p < np; p++) CK(cudaStreamWaitEvent(P0.stream, d->pipes[p].done, 0));
     float2* dst = out_dev ? (float2*)amps_out : d->out;
@@ -756,18 +766,27 @@ int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_ou
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(d->ev1, P0.stream));
+    if (trace) tB = now_ms();
     if (!out_dev) {
         CK(cudaMemcpyAsync(amps_out, d->out, d->M * sizeof(float2), cudaMemcpyDeviceToHost, P0.stream));
         CK(cudaStreamSynchronize(P0.stream));
     }
     CK(cudaEventRecord(d->evu, P0.stream));
     CK(cudaStreamWaitEvent(d->user, d->evu, 0));
+    if (trace) tC = now_ms();
     if (secs) {
-        CK(cudaEventSynchronize(d->ev1));
+        // poll instead of a blocking event wait (host wake-up latency showed up as 100s of ms outliers)
+        cudaError_t q;
+        while ((q = cudaEventQuery(d->ev1)) == cudaErrorNotReady) {
+        }
+        CK(q);
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, d->ev0, d->ev1));
         *secs = ms * 1e-3;
     }
+    if (trace)
+        fprintf(stderr, "[tn_contract] enqueue slices %.2f ms, finalize %.2f ms, tail %.2f ms, sync %.2f ms\n", tA - t0,
+                tB - tA, tC - tB, now_ms() - tC);
     return TN_OK;
 }
 
