@@ -245,7 +245,6 @@ def main():
         ev.record(stream)
         while not ev.query():
             pass
-        torch.cuda.synchronize()
 
     # ------------------------------------------------------------ end to end through the public API
     # host -> device: the step's slice ids from pinned host memory (inside tn_contract); device -> host:
