@@ -267,3 +267,50 @@ def test_config3_full_size_bench_configuration(T, oracle_built):
     want1, _ = sv.prefix_amplitudes(circ, bits, info["sliced_wires"], 1, threads=threads)
     e1, _ = assert_amps_close(got1, want1)
     print(f"config 3 prefix half: rel L2 {e1:.2e}")
+
+
+# ------------------------------------------------------------------------------ edge cases
+
+def test_edge_single_qubit_and_no_fsim(T, oracle_built):
+    """n = 1 (one tensor, no pairwise step) and a circuit whose qubits never meet (disconnected components
+    contracted by outer products, k = 0)."""
+    from oracle import sv
+    c1 = cc.generate_circuit(cc.rect_layout(1, 1), 3, "A", 5)
+    _, _, amps = run(T, c1, np.array([0, 1], np.uint64), 0, 1 << 10, n_sliced=0)
+    assert_amps_close(amps, sv.statevector(c1))
+    c2 = cc.generate_circuit(cc.rect_layout(2, 3), 2, "EE", 6)       # pattern E: few couplers
+    c2["moments"] = [m for m in c2["moments"] if all(g["type"] == "single" for g in m)] + \
+        [[{"type": "fsim", "targets": [0, 1], "theta": 1.4, "phi": 0.5}]]
+    bits = bs.all_bitstrings(6)
+    _, _, amps = run(T, c2, bits, 0, 1 << 10, n_sliced=0)
+    assert_amps_close(amps, sv.statevector(c2))
+
+
+def test_edge_all_open_and_duplicate_groups(T, oracle_built):
+    """Every qubit open (one group = the full state); duplicate fixed parts (two groups with the same bits)."""
+    from oracle import sv
+    circ = cc.generate_circuit(cc.rect_layout(2, 4), 6, "ABCDCDAB", 9)
+    n = circ["n"]
+    bits = bs.all_bitstrings(n)
+    _, _, amps = run(T, circ, bits, (1 << n) - 1, 1 << 12, n_sliced=2)
+    assert_amps_close(amps, sv.statevector(circ))
+    g = bs.generate_groups(n, [6, 7], 5, 3)
+    dup = np.concatenate([g[:4], g[:4], g[4:]])                       # group 0 repeated
+    ss, info, amps = run(T, circ, dup, bs.qubit_mask(n, [6, 7]), 1 << 12, n_sliced=2)
+    want, _ = sv.amplitudes(circ, dup)
+    assert_amps_close(amps, want)
+    np.testing.assert_array_equal(amps[:4], amps[4:8])
+
+
+def test_edge_bad_slice_subsets(T):
+    c = configs.get(2)
+    circ = c.circuit()
+    n = circ["n"]
+    ss = T.SparseState(circ, c.bitstrings(n), c.open_mask(n))
+    ss.plan(1 << c.log2_tmax, n_sliced=c.n_sliced)
+    ss.bind(0)
+    for bad in ([], [3, 3], [16], [0, 1 << 40]):
+        with pytest.raises(T.TnError) as e:
+            ss.contract(bad)
+        assert e.value.status == T.TN_EINVAL
+    ss.contract([15])  # still usable after rejected calls
