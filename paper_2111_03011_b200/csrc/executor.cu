@@ -43,13 +43,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-// 2D fp32 tensor map [rows][cols] row-major, box 128 rows x 32 cols, 128B swizzle
-bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols) {
+// 2D fp32 tensor map [rows][cols] row-major, box box_rows x 32 cols, 128B swizzle
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_rows = tc::BM) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)(cols * 4)};
-    cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)tc::BM};
+    cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -90,6 +90,7 @@ struct Launch {
     float* gC = nullptr;
     int64_t gMp = 0, gN2 = 0, gK2 = 0;
     int gEA = 0;
+    int gBN = 128;
     const int4* gTiles = nullptr;
     int gNTiles = 0, gTilesN = 1;
     const int32_t* gPerm = nullptr;
@@ -196,7 +197,9 @@ int set_smem_attrs(std::string& err) {
 #undef SETR
     CK(cudaFuncSetAttribute(kern::k_prep_a, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     CK(cudaFuncSetAttribute(kern::k_prep_b, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES));
+    CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Cfg<128>::SMEM));
+    CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Cfg<64>::SMEM));
+    CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Cfg<32>::SMEM));
     done = true;
     return TN_OK;
 }
@@ -219,9 +222,18 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
             kern::k_prep_b<<<L.grid, L.block, L.smem, st>>>(L.pb);
             break;
         case K_GEMM:
-            tc::k_gemm_tf32x3<<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp, L.gN2, L.gK2,
-                                                               L.gEA, L.gTiles, L.gPerm, L.gCm, L.gCn, L.gNTiles,
-                                                               L.gTilesN);
+            if (L.gBN == 128)
+                tc::k_gemm_tf32x3<128><<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp,
+                                                                        L.gN2, L.gK2, L.gEA, L.gTiles, L.gPerm, L.gCm,
+                                                                        L.gCn, L.gNTiles, L.gTilesN);
+            else if (L.gBN == 64)
+                tc::k_gemm_tf32x3<64><<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp,
+                                                                       L.gN2, L.gK2, L.gEA, L.gTiles, L.gPerm, L.gCm,
+                                                                       L.gCn, L.gNTiles, L.gTilesN);
+            else
+                tc::k_gemm_tf32x3<32><<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp,
+                                                                       L.gN2, L.gK2, L.gEA, L.gTiles, L.gPerm, L.gCm,
+                                                                       L.gCn, L.gNTiles, L.gTilesN);
             break;
         case K_READOUT:
             kern::k_readout<<<L.grid, L.block, 0, st>>>(L.F, L.ridx, P.acc, L.M, P.counter);
@@ -546,8 +558,11 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 const int64_t K2 = 2 * g.k;
                 const int64_t ncols = g.grouped ? g.NB * g.n : g.n;  // complex columns of the prepped B
                 const int64_t Dm = g.embed_a ? 2 * Mp : Mp, Dn = g.embed_a ? ncols : 2 * ncols;
+                // N tile: 128 real columns for wide outputs, 64 / 32 for tall-skinny ones
+                L.gBN = Dn >= 128 ? 128 : (Dn >= 64 ? 64 : 32);
+                if (g.grouped) L.gBN = 128;
                 if (!make_map(&L.tm[0], ptr(g.Ahi), Dm, K2) || !make_map(&L.tm[1], ptr(g.Alo), Dm, K2) ||
-                    !make_map(&L.tm[2], ptr(g.Bhi), Dn, K2) || !make_map(&L.tm[3], ptr(g.Blo), Dn, K2)) {
+                    !make_map(&L.tm[2], ptr(g.Bhi), Dn, K2, L.gBN) || !make_map(&L.tm[3], ptr(g.Blo), Dn, K2, L.gBN)) {
                     err = "cuTensorMapEncodeTiled failed";
                     return TN_ECUDA;
                 }
@@ -556,7 +571,7 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 L.gN2 = g.embed_a ? g.n : 2 * g.n;
                 L.gK2 = K2;
                 L.gEA = g.embed_a;
-                const int tiles_m = (int)((Dm + tc::BM - 1) / tc::BM), tiles_n = (int)(Dn / tc::BN);
+                const int tiles_m = (int)((Dm + tc::BM - 1) / tc::BM), tiles_n = (int)(Dn / L.gBN);
                 L.gNTiles = tiles_m * tiles_n;
                 // keep the larger operand's tile shared by concurrently running CTAs (read once from HBM)
                 L.gTilesN = (Dn > Dm) ? -tiles_m : tiles_n;
@@ -569,7 +584,7 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 }
                 L.grid = dim3((unsigned)std::min(L.gNTiles, 148));  // persistent: one CTA per SM
                 L.block = dim3(tc::THREADS);
-                L.smem = tc::SMEM_BYTES;
+                L.smem = L.gBN == 128 ? tc::Cfg<128>::SMEM : (L.gBN == 64 ? tc::Cfg<64>::SMEM : tc::Cfg<32>::SMEM);
             }
         } else if (st.kind == K_READOUT) {
             L.F = (const float2*)ptr(st.rp.F);
@@ -869,14 +884,14 @@ void dev_destroy(Device* d) {
 int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K, int ea, void* stream,
                std::string& err) {
     if (set_smem_attrs(err)) return TN_ECUDA;
-    if (N < 64 || K < 16 || (N & (N - 1)) || (K & (K - 1))) {
-        err = "debug_gemm: N >= 64 and K >= 16 must be powers of two";
+    if (N < 16 || K < 16 || (N & (N - 1)) || (K & (K - 1))) {
+        err = "debug_gemm: N >= 16 and K >= 16 must be powers of two";
         return TN_EINVAL;
     }
     cudaStream_t st = (cudaStream_t)stream;
     float *ahi, *alo, *bhi, *blo;
-    if (ea && N < 128) {
-        err = "debug_gemm: embedded-A mode needs N >= 128";
+    if (ea && N < 32) {
+        err = "debug_gemm: embedded-A mode needs N >= 32";
         return TN_EINVAL;
     }
     CK(cudaMalloc(&ahi, M * K * (ea ? 16 : 8)));
@@ -938,14 +953,23 @@ int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, i
     kern::k_prep_b<<<grid_for(N * K), 256, (size_t)(pb.ntn + pb.ntk) * 1024, st>>>(pb);
     CUtensorMap tm[4];
     const int64_t Dm = ea ? 2 * M : M, Dn = ea ? N : 2 * N;
-    if (!make_map(&tm[0], ahi, Dm, 2 * K) || !make_map(&tm[1], alo, Dm, 2 * K) || !make_map(&tm[2], bhi, Dn, 2 * K) ||
-        !make_map(&tm[3], blo, Dn, 2 * K)) {
+    const int bn = Dn >= 128 ? 128 : (Dn >= 64 ? 64 : 32);
+    if (!make_map(&tm[0], ahi, Dm, 2 * K) || !make_map(&tm[1], alo, Dm, 2 * K) ||
+        !make_map(&tm[2], bhi, Dn, 2 * K, bn) || !make_map(&tm[3], blo, Dn, 2 * K, bn)) {
         err = "cuTensorMapEncodeTiled failed";
         return TN_ECUDA;
     }
-    const int tiles_n = (int)(Dn / tc::BN), n_tiles = (int)(((Dm + tc::BM - 1) / tc::BM) * tiles_n);
-    tc::k_gemm_tf32x3<<<std::min(n_tiles, 148), tc::THREADS, tc::SMEM_BYTES, st>>>(
-        tm[0], tm[1], tm[2], tm[3], C, Dm, ea ? N : 2 * N, 2 * K, ea, nullptr, nullptr, 0, 0, n_tiles, tiles_n);
+    const int tiles_n = (int)(Dn / bn), n_tiles = (int)(((Dm + tc::BM - 1) / tc::BM) * tiles_n);
+    const int g = std::min(n_tiles, 148);
+    if (bn == 128)
+        tc::k_gemm_tf32x3<128><<<g, tc::THREADS, tc::Cfg<128>::SMEM, st>>>(
+            tm[0], tm[1], tm[2], tm[3], C, Dm, ea ? N : 2 * N, 2 * K, ea, nullptr, nullptr, 0, 0, n_tiles, tiles_n);
+    else if (bn == 64)
+        tc::k_gemm_tf32x3<64><<<g, tc::THREADS, tc::Cfg<64>::SMEM, st>>>(
+            tm[0], tm[1], tm[2], tm[3], C, Dm, ea ? N : 2 * N, 2 * K, ea, nullptr, nullptr, 0, 0, n_tiles, tiles_n);
+    else
+        tc::k_gemm_tf32x3<32><<<g, tc::THREADS, tc::Cfg<32>::SMEM, st>>>(
+            tm[0], tm[1], tm[2], tm[3], C, Dm, ea ? N : 2 * N, 2 * K, ea, nullptr, nullptr, 0, 0, n_tiles, tiles_n);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     cudaFree(ahi);

@@ -27,16 +27,21 @@ namespace tnb {
 namespace tc {
 
 constexpr int BM = 128;          // rows of A per tile (MMA M)
-constexpr int BN = 128;          // rows of Bt per tile (MMA N, real columns of C)
 constexpr int BK = 32;           // fp32 elements per k-block = 128 B = one swizzle atom row
-constexpr int STAGES = 3;
-constexpr int TILE_BYTES = BM * BK * 4;              // 16 KB (BM == BN)
-constexpr int STAGE_BYTES = 4 * TILE_BYTES;          // Ahi, Alo, Bhi, Blo
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int TILE_BYTES = BM * BK * 4;              // 16 KB A tile
 constexpr int THREADS = 192;
 constexpr int KSPLIT = 2;       // k-blocks alternate between KSPLIT accumulators (summed in fp32 RN):
                                 // the tensor-core accumulator truncates, so shorter chains = less bias
-constexpr int TMEM_COLS = 512;  // 2 tile buffers x KSPLIT x 128 fp32 columns
+// BN (MMA N = rows of the B tile = real output columns per tile) is a template parameter: 128 for wide
+// contractions, 64 / 32 for tall-skinny ones (long K, few output columns).
+template <int BN>
+struct Cfg {
+    static constexpr int BTILE = BN * BK * 4;                       // B tile bytes
+    static constexpr int STAGE = 2 * TILE_BYTES + 2 * BTILE;        // Ahi, Alo, Bhi, Blo
+    static constexpr int STAGES = BN == 128 ? 3 : (BN == 64 ? 4 : 5);
+    static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int TMEM_COLS = 2 * KSPLIT * BN;               // 2 tile buffers x KSPLIT x BN columns
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -103,12 +108,17 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+template <int BN>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_tf32x3(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                   const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
                   float* __restrict__ C, int64_t Mp, int64_t N2, int64_t K2, int ea,
                   const int4* __restrict__ tiles, const int32_t* __restrict__ perm, int64_t cm, int64_t cn,
                   int n_tiles, int tiles_n) {
+    constexpr int STAGES = Cfg<BN>::STAGES;
+    constexpr int STAGE_BYTES = Cfg<BN>::STAGE;
+    constexpr int TMEM_COLS = Cfg<BN>::TMEM_COLS;
+    constexpr int B0 = 2 * TILE_BYTES, B1 = 2 * TILE_BYTES + Cfg<BN>::BTILE;  // Bhi / Blo offsets
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
@@ -188,8 +198,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const int kc = kb * BK;
                     tma_load_2d(st + 0 * TILE_BYTES, &mAhi, &full[s], kc, m0);
                     tma_load_2d(st + 1 * TILE_BYTES, &mAlo, &full[s], kc, m0);
-                    tma_load_2d(st + 2 * TILE_BYTES, &mBhi, &full[s], kc, n0);
-                    tma_load_2d(st + 3 * TILE_BYTES, &mBlo, &full[s], kc, n0);
+                    tma_load_2d(st + B0, &mBhi, &full[s], kc, n0);
+                    tma_load_2d(st + B1, &mBlo, &full[s], kc, n0);
                 }
             }
         }
@@ -216,8 +226,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                         const uint32_t koff = k * 32;  // 8 tf32 = 32 B along the swizzled 128 B row
                         const uint64_t dAhi = sdesc_sw128(st + 0 * TILE_BYTES + koff);
                         const uint64_t dAlo = sdesc_sw128(st + 1 * TILE_BYTES + koff);
-                        const uint64_t dBhi = sdesc_sw128(st + 2 * TILE_BYTES + koff);
-                        const uint64_t dBlo = sdesc_sw128(st + 3 * TILE_BYTES + koff);
+                        const uint64_t dBhi = sdesc_sw128(st + B0 + koff);
+                        const uint64_t dBlo = sdesc_sw128(st + B1 + koff);
                         const uint32_t first = (kb < KSPLIT && k == 0) ? 0u : 1u;
                         mma_tf32(acc, dAlo, dBhi, idesc, first);  // small terms first
                         mma_tf32(acc, dAhi, dBlo, idesc, 1u);

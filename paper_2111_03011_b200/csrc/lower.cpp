@@ -182,7 +182,9 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         LT *A = &X, *B = &Y;
         bool grouped = false;
         if (rx && ry) {
-            if (per_row(Y) > per_row(X)) std::swap(A, B);
+            // gather-contract: the operand with FEWER rows is reused by many output rows -> M side
+            if (Y.rows.size() < X.rows.size() || (Y.rows.size() == X.rows.size() && per_row(Y) > per_row(X)))
+                std::swap(A, B);
             // gather-contract on the tensor cores when the per-row GEMMs are big enough and many output
             // rows share an A parent (grouped GEMM, see GemmParams::grouped)
             const int64_t fa = (int64_t)A->legs.size() - (int64_t)K.size();
@@ -190,14 +192,16 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             const double cm = (double)RC * std::ldexp(1.0, (int)(fa + fb + K.size()));
             const int64_t RA = (int64_t)A->rows.size();
             grouped = K.size() >= 4 && fa >= 5 && cm >= 16.0 * 1024 * 1024 &&
-                      (RC >= 16 * RA || (fa >= 10 && RC >= 2 * RA));
+                      (RC >= 16 * RA || (fa >= 7 && RC >= 2 * RA));
+            if (!grouped && per_row(*B) > per_row(*A)) std::swap(A, B);  // SIMT: stream the larger rows
             use_gemm = grouped;
         } else {
             if (ry || (!rx && per_row(Y) > per_row(X))) std::swap(A, B);
             int64_t fa = (int64_t)A->legs.size() - (int64_t)K.size();
             int64_t fb = (int64_t)B->legs.size() - (int64_t)K.size();
             int64_t m = RC << fa, n = (int64_t)1 << fb, k = (int64_t)1 << K.size();
-            use_gemm = (m >= 128 && n >= 64 && k >= 16) || (m >= 64 && n >= 128 && k >= 16);
+            use_gemm = (m >= 128 && n >= 64 && k >= 16) || (m >= 64 && n >= 128 && k >= 16) ||
+                       (m >= 128 && n >= 16 && k >= 64);  // tall-skinny, long K: N tile 32 / 64
             if (!use_gemm && per_row(*B) > per_row(*A)) std::swap(A, B);
         }
         // parent maps
@@ -393,8 +397,8 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
                 gp.n_tiles = (int64_t)tiles.size();
                 gp.tiles = BufRef{REG_MAPS, push_blob(prog.maps, tiles.data(), tiles.size() * sizeof(GemmTile))};
             } else {
-                // embed the smaller operand in the complex-as-real GEMM (its rows double)
-                gp.embed_a = (Mp < n && n >= 128) || Mp < 128 ? 1 : 0;
+                // embed the smaller operand in the complex-as-real GEMM (its rows double); EA needs n >= 32
+                gp.embed_a = ((Mp < n && n >= 128) || Mp < 128) && n >= 32 ? 1 : 0;
             }
             const int64_t abytes = (gp.embed_a ? 2 : 1) * Mp * 2 * k * 4,
                           bbytes = (gp.embed_a ? 1 : 2) * NBcols * 2 * k * 4;

@@ -88,7 +88,7 @@ inline StepCost step_cost(int a, int b, int c, int u, double rA, double rB, doub
         const bool a_is_m = rowsA || (!rowsB && sA >= sB);
         const double sM = a_is_m ? sA : sB, sN = a_is_m ? sB : sA;
         const double m = sM / std::ldexp(1.0, kk), n = sN / std::ldexp(1.0, kk);
-        s.gemm = ((m >= 128 && n >= 64) || (m >= 64 && n >= 128)) && kk >= 4;
+        s.gemm = ((m >= 128 && n >= 64) || (m >= 64 && n >= 128) || (m >= 128 && n >= 16 && kk >= 6)) && kk >= 4;
     }
     if (s.gemm) {
         // pre-passes read both operands and write hi + lo (the smaller one embedded, 2x), the GEMM reads

@@ -158,7 +158,8 @@ def test_forced_wires_and_tight_bound(T, oracle_built):
 # ------------------------------------------------------------------------------ tensor-core GEMM unit
 
 @pytest.mark.parametrize("M,N,K,ea", [(128, 64, 16, 0), (1000, 128, 64, 0), (4096, 256, 512, 0), (333, 64, 1024, 0),
-                                      (128, 128, 16, 1), (77, 256, 64, 1), (1000, 512, 512, 1)])
+                                      (128, 128, 16, 1), (77, 256, 64, 1), (1000, 512, 512, 1),
+                                      (3000, 16, 256, 0), (500, 32, 1024, 0), (700, 32, 128, 1), (256, 64, 64, 1)])
 def test_tcgen05_gemm_3xtf32(T, M, N, K, ea):
     """The tcgen05 3xTF32 complex GEMM against fp64 numpy: relative error at fp32 level."""
     import torch
