@@ -180,7 +180,10 @@ def main():
     ss = T.SparseState(circ, bits, cfg.open_mask(n))
     t_build = time.perf_counter() - t0
     t0 = time.perf_counter()
-    info = ss.plan(1 << cfg.log2_tmax, n_sliced=cfg.n_sliced, seed=1, trials=args.trials)
+    pk = cfg.plan_kwargs()
+    if args.trials:
+        pk["trials"] = args.trials
+    info = ss.plan(1 << cfg.log2_tmax, **pk)
     t_plan = time.perf_counter() - t0
     if world > 1:  # every rank must contract the same sliced network: compare plan fingerprints
         fp = torch.tensor([float(hash(tuple(info["sliced_wires"])) % (1 << 52)), info["cmac_per_slice"]],

@@ -255,7 +255,7 @@ def test_config3_full_size_bench_configuration(T, oracle_built):
     n = circ["n"]
     bits = c.bitstrings(n)
     ss = T.SparseState(circ, bits, c.open_mask(n))
-    info = ss.plan(1 << c.log2_tmax, n_sliced=c.n_sliced, seed=1)
+    info = ss.plan(1 << c.log2_tmax, **c.plan_kwargs())   # the plan bench.py times
     ss.bind(0, pipelines=16)
     s = info["s"]
     got = ss.contract(range(1 << s)).cpu().numpy()

@@ -29,6 +29,10 @@ class Config:
     open_qubits: Optional[List[int]] = None
     final_layer: bool = True
     note: str = ""
+    # planner settings (plan search is setup; chosen by measuring candidate plans, tools/plan_sweep.py)
+    plan_seed: int = 1
+    plan_trials: int = 0
+    plan_budget_s: float = 0.0
 
     def qubits(self):
         if self.layout == "sycamore53":
@@ -48,6 +52,10 @@ class Config:
     def bitstrings(self, n: int, seed: Optional[int] = None):
         return bs.generate_groups(n, self.open_ids(n), self.L, 2000 + self.cfg if seed is None else seed)
 
+    def plan_kwargs(self) -> dict:
+        return {"n_sliced": self.n_sliced, "seed": self.plan_seed, "trials": self.plan_trials,
+                "time_budget_s": self.plan_budget_s}
+
     def open_mask(self, n: int) -> int:
         return bs.qubit_mask(n, self.open_ids(n))
 
@@ -62,7 +70,7 @@ CONFIGS = {
     2: Config(2, "20q-m8", "rect:4x5", 8, SUPREMACY, L=64, n_open=6, n_sliced=4, log2_tmax=20,
               note="2^4 slices all contracted"),
     3: Config(3, "30q-m12", "rect:5x6", 12, SUPREMACY, L=1024, n_open=6, n_sliced=8, log2_tmax=28,
-              note="2^8 slices, fraction sweep"),
+              note="2^8 slices, fraction sweep", plan_seed=3, plan_trials=96, plan_budget_s=120.0),
     4: Config(4, "53q-m14", "sycamore53", 14, SUPREMACY, L=1 << 14, n_open=6, n_sliced=12, log2_tmax=32,
               open_qubits=[11, 19, 28, 29, 37, 44], note="2^12 slices over 1/2/4/8 GPUs"),
     5: Config(5, "53q-m20", "sycamore53", 20, SUPREMACY, L=1 << 20, n_open=6, n_sliced=-1, log2_tmax=32,

@@ -21,7 +21,7 @@ circ = c.circuit()
 n = circ["n"]
 bits = c.bitstrings(n)
 ss = T.SparseState(circ, bits, c.open_mask(n))
-info = ss.plan(1 << c.log2_tmax, n_sliced=c.n_sliced, seed=1)
+info = ss.plan(1 << c.log2_tmax, **c.plan_kwargs())
 ss.bind(local)
 S = list(range(1 << info["s"]))
 amps = contract_distributed(ss, S).cpu().numpy()

@@ -15,7 +15,7 @@ c = configs.get(3)
 circ = c.circuit()
 n = circ["n"]
 ss = T.SparseState(circ, c.bitstrings(n), c.open_mask(n))
-info = ss.plan(1 << c.log2_tmax, n_sliced=c.n_sliced, seed=1)
+info = ss.plan(1 << c.log2_tmax, **c.plan_kwargs())
 ss.bind(0, pipelines=16)
 ids = list(range(256))
 out = torch.empty(ss.M, dtype=torch.complex64, device="cuda")

@@ -14,7 +14,7 @@ c = configs.get(cfg)
 circ = c.circuit()
 n = circ["n"]
 ss = T.SparseState(circ, c.bitstrings(n), c.open_mask(n))
-info = ss.plan(1 << c.log2_tmax, n_sliced=c.n_sliced, seed=1)
+info = ss.plan(1 << c.log2_tmax, **c.plan_kwargs())
 ss.bind(0)
 amps = ss.contract(range(ns))
 torch.cuda.synchronize()

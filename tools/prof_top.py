@@ -13,7 +13,7 @@ c = configs.get(cfg)
 circ = c.circuit()
 n = circ["n"]
 ss = T.SparseState(circ, c.bitstrings(n), c.open_mask(n))
-info = ss.plan(1 << c.log2_tmax, n_sliced=c.n_sliced, seed=1)
+info = ss.plan(1 << c.log2_tmax, **c.plan_kwargs())
 print({k: v for k, v in info.items() if k != "sliced_wires"})
 ss.bind(0)
 ss.contract([0])
