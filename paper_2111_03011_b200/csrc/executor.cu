@@ -192,7 +192,8 @@ int set_smem_attrs(std::string& err) {
     SETA(0, 1); SETA(1, 1); SETA(2, 1); SETA(3, 1); SETA(4, 1);
     SETA(0, 32); SETA(1, 32); SETA(2, 32); SETA(3, 32); SETA(4, 32);
 #undef SETA
-#define SETR(NI) CK(cudaFuncSetAttribute(kern::k_apply_rows<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, big))
+#define SETR(NI) CK(cudaFuncSetAttribute(kern::k_apply_rows<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         kern::ROWS_SMEM_MAX))
     SETR(0); SETR(1); SETR(2); SETR(3); SETR(4);
 #undef SETR
     CK(cudaFuncSetAttribute(kern::k_prep_a, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
@@ -472,8 +473,9 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                          (p.n_orbits * L.team) % 256 == 0) ? 1 : 0;
             if (p.stage_b) L.smem += (size_t)a.b_row * 8;
             // gather-contract with small parent rows: one block per output row, rows staged in smem
+            const size_t rows_smem = (size_t)p.ntab * 256 * 4 * 4 + ((size_t)8 << a.nk) + (size_t)(a.a_row + a.b_row) * 8;
             if (a.nk <= kern::KTAB_MAX_BITS && (a.ma.region != REG_NONE || a.mb.region != REG_NONE) &&
-                a.a_row + a.b_row <= 12288 && a.R >= 128) {
+                rows_smem <= kern::ROWS_SMEM_MAX && a.R >= 128) {
                 L.rows_mode = 1;
                 p.stage_b = 0;
                 int kp = 1;

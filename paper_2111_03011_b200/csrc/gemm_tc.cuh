@@ -129,6 +129,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nkb = (int)(K2 / BK);
+    // grouped scatter: cm (rows per output row-block) and cn (columns) are powers of two
+    const int lcm = 63 - __clzll(cm > 0 ? cm : 1), lcn = 63 - __clzll(cn > 0 ? cn : 1);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
@@ -289,9 +291,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 const int c = c0 + 2 * q;
                                 if (c >= yvalid) break;
                                 const int64_t j = (int64_t)(n0 - ybase + c) >> 1;
-                                const int64_t pblk = goff + j / cn, fb = j % cn;
+                                const int64_t pblk = goff + (j >> lcn), fb = j & (cn - 1);
                                 const int64_t r = perm[pblk];
-                                *(float2*)(C + 2 * ((r * cm + fa) * cn + fb)) =
+                                *(float2*)(C + 2 * ((((r << lcm) + fa) << lcn) + fb)) =
                                     make_float2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
                             }
                         }
@@ -311,11 +313,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 const int c = c0 + (odd ? 16 : 0) + q;
                                 if (c >= yvalid) break;
                                 const int64_t j = (int64_t)(n0 - ybase + c);
-                                const int64_t pblk = goff + j / cn, fb = j % cn;
+                                const int64_t pblk = goff + (j >> lcn), fb = j & (cn - 1);
                                 const int64_t r = perm[pblk];
                                 const float re = odd ? y[q] : __uint_as_float(v[q]);
                                 const float im = odd ? __uint_as_float(v[16 + q]) : y[q];
-                                *(float2*)(C + 2 * ((r * cm + fa) * cn + fb)) = make_float2(re, im);
+                                *(float2*)(C + 2 * ((((r << lcm) + fa) << lcn) + fb)) = make_float2(re, im);
                             }
                         }
                     }

@@ -66,6 +66,7 @@ struct ApplyDev {
 };
 constexpr int KTAB_MAX_BITS = 12;
 constexpr int STAGE_B_MAX = 4096;  // complex elements of B per row staged in shared memory
+constexpr int ROWS_SMEM_MAX = 112 * 1024;  // k_apply_rows: tables + both parent rows in shared memory (>= 2 CTAs/SM)
 
 template <int NI, int TEAM>
 __global__ void __launch_bounds__(256) k_apply(const ApplyDev p) {
