@@ -84,6 +84,7 @@ struct Launch {
     kern::ApplyDev ap;
     int ni = 0, team = 1;
     int rows_mode = 0;  // k_apply_rows (row-staged gather-contract)
+    int na = 0;         // k_apply_na: orbits per thread = 2^na
     kern::PrepADev pa;
     kern::PrepBDev pb;
     CUtensorMap tm[4];
@@ -158,6 +159,21 @@ void launch_apply(const Launch& L, cudaStream_t st) {
     kern::k_apply<NI, TEAM><<<L.grid, L.block, L.smem, st>>>(L.ap);
 }
 
+template <int NI, int NA>
+void launch_apply_na(const Launch& L, cudaStream_t st) {
+    kern::k_apply_na<NI, NA><<<L.grid, L.block, L.smem, st>>>(L.ap);
+}
+
+template <int NA>
+void launch_apply_na_ni(const Launch& L, cudaStream_t st) {
+    switch (L.ni) {
+        case 0: launch_apply_na<0, NA>(L, st); break;
+        case 1: launch_apply_na<1, NA>(L, st); break;
+        case 2: launch_apply_na<2, NA>(L, st); break;
+        default: launch_apply_na<3, NA>(L, st); break;
+    }
+}
+
 template <int NI>
 void launch_apply_rows(const Launch& L, cudaStream_t st) {
     kern::k_apply_rows<NI><<<L.grid, L.block, L.smem, st>>>(L.ap);
@@ -192,6 +208,10 @@ int set_smem_attrs(std::string& err) {
     SETA(0, 1); SETA(1, 1); SETA(2, 1); SETA(3, 1); SETA(4, 1);
     SETA(0, 32); SETA(1, 32); SETA(2, 32); SETA(3, 32); SETA(4, 32);
 #undef SETA
+#define SETN(NI, NA) CK(cudaFuncSetAttribute(kern::k_apply_na<NI, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, big))
+    SETN(0, 1); SETN(1, 1); SETN(2, 1); SETN(3, 1);
+    SETN(0, 2); SETN(1, 2); SETN(2, 2); SETN(3, 2);
+#undef SETN
 #define SETR(NI) CK(cudaFuncSetAttribute(kern::k_apply_rows<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                          kern::ROWS_SMEM_MAX))
     SETR(0); SETR(1); SETR(2); SETR(3); SETR(4);
@@ -212,7 +232,9 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
                                                             P.work, P.slice_ids, P.counter, d->s);
             break;
         case K_APPLY:
-            if (L.rows_mode) launch_apply_rows_ni(L, st);
+            if (L.na == 1) launch_apply_na_ni<1>(L, st);
+            else if (L.na == 2) launch_apply_na_ni<2>(L, st);
+            else if (L.rows_mode) launch_apply_rows_ni(L, st);
             else if (L.team == 32) launch_apply_ni<32>(L, st);
             else launch_apply_ni<1>(L, st);
             break;
@@ -250,7 +272,7 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
 std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
     auto small = [](const Launch& L) {
         return L.kind == K_APPLY && L.ap.ktab != nullptr && L.ap.R * L.ap.n_orbits <= 65536 && L.cmac <= 4.0e6 &&
-               !L.ap.stage_b && !L.rows_mode;
+               !L.ap.stage_b && !L.rows_mode && !L.na;
     };
     auto ov = [](const void* a, int64_t na, const void* b, int64_t nb) {
         const char* x = (const char*)a;
@@ -409,9 +431,38 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
             for (int i = 0; i < a.cB.n; i++) b_of_c[a.cB.dst[i]] = a.cB.src[i];
             std::vector<bool> inner(a.dC, false);
             for (int u = 0; u < a.n_inner; u++) inner[a.inner_c[u]] = true;
+            // register blocking (k_apply_na): up to 2 A-free C bits, above the lowest 6 orbit bits (the lane
+            // bits, kept for coalescing), become per-thread bits when the step is big and k fits the table
+            std::vector<int> na_bits;
+            {
+                std::vector<int> cand;
+                int seen = 0;
+                for (int c = 0; c < a.dC; c++) {
+                    if (inner[c]) continue;
+                    if (seen++ < 6) continue;
+                    if (a_of_c[c] >= 0) cand.push_back(c);
+                }
+                const int64_t orbits_all = (int64_t)1 << (a.dC - a.n_inner);
+                const int want = (a.nk <= kern::KTAB_MAX_BITS && a.n_inner <= 3 && a.R * orbits_all >= (1 << 16))
+                                     ? std::min(2, 5 - a.n_inner) : 0;
+                for (int t = 0; t < want && t < (int)cand.size(); t++) na_bits.push_back(cand[cand.size() - 1 - t]);
+            }
+            for (int c : na_bits) inner[c] = true;  // excluded from the orbit index
             std::vector<int> orb;  // orbit bit t -> C bit
             for (int c = 0; c < a.dC; c++)
                 if (!inner[c]) orb.push_back(c);
+            for (int c : na_bits) inner[c] = false;
+            L.na = (int)na_bits.size();
+            for (int j = 0; j < (1 << L.na); j++) {
+                uint32_t ao = 0, co = 0;
+                for (int u = 0; u < L.na; u++)
+                    if ((j >> u) & 1) {
+                        ao += 1u << a_of_c[na_bits[u]];
+                        co += 1u << na_bits[u];
+                    }
+                p.a_extra[j] = ao;
+                p.c_extra[j] = co;
+            }
             const int nob = (int)orb.size();
             p.n_orbits = (int64_t)1 << nob;
             p.ntab = (nob + 7) / 8;
@@ -471,10 +522,15 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
             L.smem = (size_t)p.ntab * 256 * 4 * 4 + (a.nk <= kern::KTAB_MAX_BITS ? ((size_t)8 << a.nk) : 0);
             p.stage_b = (a.nk <= kern::KTAB_MAX_BITS && a.b_row <= kern::STAGE_B_MAX &&
                          (p.n_orbits * L.team) % 256 == 0) ? 1 : 0;
+            if (L.na) {  // register-blocked path: TEAM = 1, B through L1, no row staging
+                L.team = 1;
+                p.stage_b = 0;
+                L.grid = grid_for(total, 256, 148 * 8);
+            }
             if (p.stage_b) L.smem += (size_t)a.b_row * 8;
             // gather-contract with small parent rows: one block per output row, rows staged in smem
             const size_t rows_smem = (size_t)p.ntab * 256 * 4 * 4 + ((size_t)8 << a.nk) + (size_t)(a.a_row + a.b_row) * 8;
-            if (a.nk <= kern::KTAB_MAX_BITS && (a.ma.region != REG_NONE || a.mb.region != REG_NONE) &&
+            if (!L.na && a.nk <= kern::KTAB_MAX_BITS && (a.ma.region != REG_NONE || a.mb.region != REG_NONE) &&
                 rows_smem <= kern::ROWS_SMEM_MAX && a.R >= 128) {
                 L.rows_mode = 1;
                 p.stage_b = 0;

@@ -63,6 +63,7 @@ struct ApplyDev {
     uint32_t inner_c[16], inner_b[16];
     int stage_b;           // 1: a 256-thread chunk lies in one output row; B's row is staged in smem
     int kparts;            // k_apply_rows: lanes sharing one orbit (power of two <= 32)
+    uint32_t a_extra[4], c_extra[4];  // k_apply_na: offsets of the per-thread A-free C bits
 };
 constexpr int KTAB_MAX_BITS = 12;
 constexpr int STAGE_B_MAX = 4096;  // complex elements of B per row staged in shared memory
@@ -192,6 +193,59 @@ __global__ void __launch_bounds__(256) k_apply(const ApplyDev p) {
 #pragma unroll
             for (int ii = 0; ii < (1 << NI); ii++) Cr[p.inner_c[ii]] = acc[ii];
         }
+    }
+}
+
+// ---------------------------------------------------------------------------- register-blocked apply
+// (row a5) as k_apply with TEAM = 1, but every thread owns 2^NA orbits that differ only in A-free bits
+// (above the lane bits, so loads stay coalesced): each B value loaded feeds 2^NA x more FMAs.
+template <int NI, int NA>
+__global__ void __launch_bounds__(256) k_apply_na(const ApplyDev p) {
+    extern __shared__ uint32_t sm[];
+    const int tabn = p.ntab * 256 * 4;
+    for (int i = threadIdx.x; i < tabn; i += blockDim.x) sm[i] = p.tab[i];
+    uint32_t* sk = sm + tabn;
+    const int kn = 2 << p.nk;
+    for (int i = threadIdx.x; i < kn; i += blockDim.x) sk[i] = p.ktab[i];
+    __syncthreads();
+    const int64_t K = (int64_t)1 << p.nk;
+    const int64_t total = p.R * p.n_orbits;
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = w / p.n_orbits;
+        const int64_t o = w - r * p.n_orbits;
+        uint32_t coff = 0, aoff = 0, boff = 0;
+        for (int t = 0; t < p.ntab; t++) {
+            const uint32_t* e = sm + ((t << 8) + (int)((o >> (8 * t)) & 255)) * 4;
+            coff += e[0];
+            aoff += e[1];
+            boff += e[2];
+        }
+        const int64_t ra = p.ma ? (int64_t)p.ma[r] : r;
+        const int64_t rb = p.mb ? (int64_t)p.mb[r] : 0;
+        const float2* __restrict__ Ar = p.A + ra * p.a_row + aoff;
+        const float2* __restrict__ Br = p.B + rb * p.b_row + boff;
+        float2 acc[1 << NA][1 << NI];
+#pragma unroll
+        for (int j = 0; j < (1 << NA); j++)
+#pragma unroll
+            for (int ii = 0; ii < (1 << NI); ii++) acc[j][ii] = make_float2(0.f, 0.f);
+        for (int64_t kk = 0; kk < K; kk++) {
+            const uint32_t ka = sk[2 * kk], kb = sk[2 * kk + 1];
+            float2 a[1 << NA];
+#pragma unroll
+            for (int j = 0; j < (1 << NA); j++) a[j] = Ar[ka + p.a_extra[j]];
+#pragma unroll
+            for (int ii = 0; ii < (1 << NI); ii++) {
+                const float2 b = Br[kb + p.inner_b[ii]];
+#pragma unroll
+                for (int j = 0; j < (1 << NA); j++) acc[j][ii] = cmac(acc[j][ii], a[j], b);
+            }
+        }
+        float2* Cr = p.C + r * p.c_row + coff;
+#pragma unroll
+        for (int j = 0; j < (1 << NA); j++)
+#pragma unroll
+            for (int ii = 0; ii < (1 << NI); ii++) Cr[p.c_extra[j] + p.inner_c[ii]] = acc[j][ii];
     }
 }
 
