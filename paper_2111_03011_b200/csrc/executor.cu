@@ -85,6 +85,8 @@ struct Launch {
     int ni = 0, team = 1;
     int rows_mode = 0;  // k_apply_rows (row-staged gather-contract)
     int na = 0;         // k_apply_na: orbits per thread = 2^na
+    int rg = 0, rg_fat = 0, rg_fb = 0;  // k_apply_rg<FAT, FB> (row GEMM)
+    kern::RowGemmDev rgp;
     kern::PrepADev pa;
     kern::PrepBDev pb;
     CUtensorMap tm[4];
@@ -179,6 +181,51 @@ void launch_apply_rows(const Launch& L, cudaStream_t st) {
     kern::k_apply_rows<NI><<<L.grid, L.block, L.smem, st>>>(L.ap);
 }
 
+template <int FAT, int FB>
+void launch_rg(const Launch& L, cudaStream_t st) {
+    if constexpr (FAT + FB <= 5) kern::k_apply_rg<FAT, FB><<<L.grid, L.block, L.smem, st>>>(L.rgp);
+}
+
+template <int FAT>
+void launch_rg_fb(const Launch& L, cudaStream_t st) {
+    switch (L.rg_fb) {
+        case 0: launch_rg<FAT, 0>(L, st); break;
+        case 1: launch_rg<FAT, 1>(L, st); break;
+        case 2: launch_rg<FAT, 2>(L, st); break;
+        case 3: launch_rg<FAT, 3>(L, st); break;
+        case 4: launch_rg<FAT, 4>(L, st); break;
+        default: launch_rg<FAT, 5>(L, st); break;
+    }
+}
+
+void launch_rg_any(const Launch& L, cudaStream_t st) {
+    switch (L.rg_fat) {
+        case 0: launch_rg_fb<0>(L, st); break;
+        case 1: launch_rg_fb<1>(L, st); break;
+        case 2: launch_rg_fb<2>(L, st); break;
+        case 3: launch_rg_fb<3>(L, st); break;
+        case 4: launch_rg_fb<4>(L, st); break;
+        default: launch_rg_fb<5>(L, st); break;
+    }
+}
+
+template <int FAT, int FB>
+cudaError_t set_rg_attr() {
+    if constexpr (FAT + FB <= 5)
+        return cudaFuncSetAttribute(kern::k_apply_rg<FAT, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kern::RG_SMEM_MAX);
+    return cudaSuccess;
+}
+
+template <int FAT>
+cudaError_t set_rg_attrs_fb() {
+    cudaError_t e = cudaSuccess;
+    for (cudaError_t x : {set_rg_attr<FAT, 0>(), set_rg_attr<FAT, 1>(), set_rg_attr<FAT, 2>(), set_rg_attr<FAT, 3>(),
+                          set_rg_attr<FAT, 4>(), set_rg_attr<FAT, 5>()})
+        if (x != cudaSuccess) e = x;
+    return e;
+}
+
 void launch_apply_rows_ni(const Launch& L, cudaStream_t st) {
     switch (L.ni) {
         case 0: launch_apply_rows<0>(L, st); break;
@@ -216,6 +263,8 @@ int set_smem_attrs(std::string& err) {
                                          kern::ROWS_SMEM_MAX))
     SETR(0); SETR(1); SETR(2); SETR(3); SETR(4);
 #undef SETR
+    CK(set_rg_attrs_fb<0>()); CK(set_rg_attrs_fb<1>()); CK(set_rg_attrs_fb<2>());
+    CK(set_rg_attrs_fb<3>()); CK(set_rg_attrs_fb<4>()); CK(set_rg_attrs_fb<5>());
     CK(cudaFuncSetAttribute(kern::k_prep_a, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     CK(cudaFuncSetAttribute(kern::k_prep_b, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Cfg<128>::SMEM));
@@ -232,7 +281,8 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
                                                             P.work, P.slice_ids, P.counter, d->s);
             break;
         case K_APPLY:
-            if (L.na == 1) launch_apply_na_ni<1>(L, st);
+            if (L.rg) launch_rg_any(L, st);
+            else if (L.na == 1) launch_apply_na_ni<1>(L, st);
             else if (L.na == 2) launch_apply_na_ni<2>(L, st);
             else if (L.rows_mode) launch_apply_rows_ni(L, st);
             else if (L.team == 32) launch_apply_ni<32>(L, st);
@@ -272,7 +322,7 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
 std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
     auto small = [](const Launch& L) {
         return L.kind == K_APPLY && L.ap.ktab != nullptr && L.ap.R * L.ap.n_orbits <= 65536 && L.cmac <= 4.0e6 &&
-               !L.ap.stage_b && !L.rows_mode && !L.na;
+               !L.ap.stage_b && !L.rows_mode && !L.na && !L.rg;
     };
     auto ov = [](const void* a, int64_t na, const void* b, int64_t nb) {
         const char* x = (const char*)a;
@@ -541,6 +591,99 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 L.smem = (size_t)p.ntab * 256 * 4 * 4 + ((size_t)8 << a.nk) + (size_t)(a.a_row + a.b_row) * 8;
                 L.grid = dim3((unsigned)std::min<int64_t>(a.R, 148 * 8));
             }
+            // row GEMM: long k, few outputs per row, B's row small enough to stage (k_apply_rg)
+            {
+                const char* ev = getenv("TNB_RG");  // TEMP experiment knob: 0 off, 1 default, 2 over rows mode
+                const int rgm = ev ? atoi(ev) : 1;
+                const int fa = a.cA.n, fb = a.cB.n;
+                const int FB = fb, FAT = std::min(fa, 5 - FB), g = fa - FAT;
+                if (rgm && fa + fb == a.dC && a.nk >= 6 && a.nk <= kern::KTAB_MAX_BITS && FB <= 5 && FAT >= 0 &&
+                    FAT + FB >= 1 && g <= 3 && a.R >= 64 && a.b_row >= 16 && a.b_row <= 8192 &&
+                    a.a_row >= a.b_row && st.cmac > 4.0e6 && !L.na && (rgm == 2 || !L.rows_mode)) {
+                    L.rg = 1;
+                    L.rows_mode = 0;
+                    L.team = 1;
+                    L.rg_fat = FAT;
+                    L.rg_fb = FB;
+                    kern::RowGemmDev& q = L.rgp;
+                    std::memset(&q, 0, sizeof(q));
+                    q.A = p.A;
+                    q.B = p.B;
+                    q.C = p.C;
+                    q.ma = p.ma;
+                    q.mb = p.mb;
+                    q.R = a.R;
+                    q.a_row = a.a_row;
+                    q.b_row = a.b_row;
+                    q.c_row = a.c_row;
+                    q.nk = a.nk;
+                    q.fa = fa;
+                    q.g = g;
+                    // k enumerated with A's lowest contracted bits first: the lanes read A in full sectors
+                    std::vector<std::pair<int, int>> kord;
+                    for (int t = 0; t < a.nk; t++) kord.push_back({a.kA[t], a.kB[t]});
+                    std::sort(kord.begin(), kord.end());
+                    // smem swizzle: the lanes' B bits at or above the 4 bank bits of a float2 are folded onto
+                    // the bank bits no lane bit already varies
+                    std::vector<int> lane_b;
+                    for (int t = 0; t < 5 && t < a.nk; t++) lane_b.push_back(kord[t].second);
+                    std::vector<int> freeb, src;
+                    for (int b = 0; b < 4; b++)
+                        if (std::find(lane_b.begin(), lane_b.end(), b) == lane_b.end()) freeb.push_back(b);
+                    for (int b : lane_b)
+                        if (b >= 4) src.push_back(b);
+                    q.nswz = (int)std::min(freeb.size(), src.size());
+                    for (int t = 0; t < q.nswz; t++) {
+                        q.swz_src[t] = src[t];
+                        q.swz_dst[t] = freeb[t];
+                    }
+                    auto swz = [&](uint32_t x) {
+                        uint32_t y = x;
+                        for (int t = 0; t < q.nswz; t++) y ^= ((x >> q.swz_src[t]) & 1u) << q.swz_dst[t];
+                        return y;
+                    };
+                    tabs.resize((tabs.size() + 3) & ~(size_t)3, 0);
+                    const size_t kb0 = tabs.size();
+                    tabs.resize(kb0 + ((size_t)2 << a.nk), 0);
+                    for (int64_t kk = 0; kk < ((int64_t)1 << a.nk); kk++) {
+                        uint32_t ka = 0, kb = 0;
+                        for (int t = 0; t < a.nk; t++)
+                            if ((kk >> t) & 1) {
+                                ka += 1u << kord[t].first;
+                                kb += 1u << kord[t].second;
+                            }
+                        tabs[kb0 + 2 * kk] = ka;
+                        tabs[kb0 + 2 * kk + 1] = swz(kb);
+                    }
+                    fixes.push_back({P.launches.size(), 4, kb0});
+                    tabs.resize((tabs.size() + 3) & ~(size_t)3, 0);
+                    const size_t f0 = tabs.size();
+                    for (int i = 0; i < (1 << fa); i++) {
+                        uint32_t ao = 0, co = 0;
+                        for (int u = 0; u < fa; u++)
+                            if ((i >> u) & 1) {
+                                ao += 1u << a.cA.src[u];
+                                co += 1u << a.cA.dst[u];
+                            }
+                        tabs.push_back(ao);
+                        tabs.push_back(co);
+                    }
+                    for (int j = 0; j < (1 << FB); j++) {
+                        uint32_t bo = 0, co = 0;
+                        for (int u = 0; u < fb; u++)
+                            if ((j >> u) & 1) {
+                                bo += 1u << a.cB.src[u];
+                                co += 1u << a.cB.dst[u];
+                            }
+                        tabs.push_back(swz(bo));
+                        tabs.push_back(co);
+                    }
+                    fixes.push_back({P.launches.size(), 5, f0});
+                    L.smem = (size_t)a.b_row * 8 + ((size_t)8 << a.nk) + (((size_t)2 << fa) + ((size_t)2 << FB)) * 4 +
+                             8 * ((size_t)8 << (FAT + FB));
+                    L.grid = dim3((unsigned)std::min<int64_t>(a.R, 148 * 2));
+                }
+            }
             L.a_bytes = a.a_elems * 8;
             L.b_bytes = a.b_elems * 8;
             L.c_bytes = a.R * a.c_row * 8;
@@ -662,7 +805,9 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
         if (f.which == 0) L.ap.tab = p;
         else if (f.which == 1) L.ap.ktab = p;
         else if (f.which == 2) L.pa.tab = p;
-        else L.pb.tab = p;
+        else if (f.which == 3) L.pb.tab = p;
+        else if (f.which == 4) L.rgp.ktab = p;
+        else L.rgp.ftab = p;
     }
 
     P.launches = fuse_small(P, P.launches);
@@ -684,7 +829,14 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
     CK(cudaMemset(P.slice_ids, 0, P.slice_cap * sizeof(uint64_t)));
     CK(cudaMemset(P.counter, 0, sizeof(int64_t)));
     CK(cudaStreamBeginCapture(P.stream, cudaStreamCaptureModeThreadLocal));
-    for (const Launch& L : P.launches) do_launch(d, P, L, P.stream);
+    // TEMP experiment knob: TNB_SKIP="k2,k3,s56" drops launches of kind 2, 3 and of step 56 from the graph
+    std::string skip = getenv("TNB_SKIP") ? std::string(",") + getenv("TNB_SKIP") + "," : std::string();
+    for (const Launch& L : P.launches) {
+        if (!skip.empty() && (skip.find(",k" + std::to_string(L.kind) + ",") != std::string::npos ||
+                              skip.find(",s" + std::to_string(L.pair) + ",") != std::string::npos))
+            continue;
+        do_launch(d, P, L, P.stream);
+    }
     cudaError_t ce = cudaStreamEndCapture(P.stream, &P.graph);
     if (ce != cudaSuccess) {
         err = std::string("graph capture failed: ") + cudaGetErrorString(ce);

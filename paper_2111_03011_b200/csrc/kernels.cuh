@@ -67,6 +67,7 @@ struct ApplyDev {
 };
 constexpr int KTAB_MAX_BITS = 12;
 constexpr int STAGE_B_MAX = 4096;  // complex elements of B per row staged in shared memory
+constexpr int RG_SMEM_MAX = 100 * 1024;   // k_apply_rg: B row (<= 8192 complex) + tables + reduction buffer
 constexpr int ROWS_SMEM_MAX = 112 * 1024;  // k_apply_rows: tables + both parent rows in shared memory (>= 2 CTAs/SM)
 
 template <int NI, int TEAM>
@@ -396,6 +397,130 @@ __global__ void __launch_bounds__(256) k_multi(const MStep* __restrict__ steps, 
         if (threadIdx.x == 0) {
             __threadfence();
             atomicAdd(&done[s_step], 1);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- row GEMM (rows a5/a6)
+// Gather-contract with long k and few outputs per row:
+//   C[r][cA(i) + cB(j)] = sum_kk A[ma[r]][aK(kk) + aF(i)] * B[mb[r]][bK(kk) + bF(j)]
+// One CTA per output row: B's row is staged in shared memory (XOR-swizzled so that the lanes' B
+// addresses hit distinct banks), A's row is streamed once from HBM with lanes walking A's lowest
+// contracted bits (full sectors).  Thread group g (2^G groups of 256/2^G threads) owns the A-free
+// combos [g*2^FAT, (g+1)*2^FAT); every thread accumulates its 2^FAT x 2^FB outputs over its share
+// of k, then a recursive-halving warp reduction and a shared-memory sum over the group's warps.
+struct RowGemmDev {
+    const float2* A;
+    const float2* B;
+    float2* C;
+    const int32_t* ma;
+    const int32_t* mb;
+    int64_t R, a_row, b_row, c_row;
+    const uint32_t* ktab;  // [2^nk][2] = (A offset, swizzled B offset), kk bit t = t-th lowest A k-bit
+    const uint32_t* ftab;  // [2^fa][2] = (A offset, C offset) of the A-free combos, then [2^FB][2] = (swz B, C)
+    int nk, fa, g;
+    int nswz;
+    int swz_src[4], swz_dst[4];  // B staging swizzle: bit dst of the smem index ^= bit src
+};
+
+template <int FAT, int FB>
+__global__ void __launch_bounds__(256, 2) k_apply_rg(const RowGemmDev p) {
+    constexpr int NA = 1 << FAT, NB = 1 << FB, NV = NA * NB;
+    static_assert(NV <= 32, "at most 32 complex accumulators per thread");
+    extern __shared__ __align__(16) float2 smf[];
+    float2* sB = smf;
+    uint32_t* sK = (uint32_t*)(sB + p.b_row);
+    const int kn = 2 << p.nk;
+    uint32_t* sF = sK + kn;
+    const int fn = (2 << p.fa) + 2 * NB;
+    float2* red = (float2*)(sF + fn);  // [8 warps][NV]
+    for (int i = threadIdx.x; i < kn; i += 256) sK[i] = p.ktab[i];
+    for (int i = threadIdx.x; i < fn; i += 256) sF[i] = p.ftab[i];
+    const int tpg = 256 >> p.g;
+    const int grp = threadIdx.x / tpg, tg = threadIdx.x % tpg;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int K = 1 << p.nk;
+    for (int64_t r = blockIdx.x; r < p.R; r += gridDim.x) {
+        const int64_t ra = p.ma ? (int64_t)p.ma[r] : r;
+        const int64_t rb = p.mb ? (int64_t)p.mb[r] : 0;
+        __syncthreads();  // the previous row is done with sB / red (and the tables are loaded)
+        {
+            const float4* src = (const float4*)(p.B + rb * p.b_row);
+            for (int i = threadIdx.x; i < (int)(p.b_row >> 1); i += 256) {
+                const float4 v = __ldg(src + i);
+                int e = 2 * i, x = 0;
+                for (int t = 0; t < p.nswz; t++) x |= ((e >> p.swz_src[t]) & 1) << p.swz_dst[t];
+                // swizzle sources are bits >= 4, so e and e + 1 share x
+                sB[e ^ x] = make_float2(v.x, v.y);
+                sB[(e + 1) ^ x] = make_float2(v.z, v.w);
+            }
+        }
+        __syncthreads();
+        uint32_t aoff[NA], boff[NB];
+#pragma unroll
+        for (int i = 0; i < NA; i++) aoff[i] = sF[2 * ((grp << FAT) + i)];
+#pragma unroll
+        for (int j = 0; j < NB; j++) boff[j] = sF[(2 << p.fa) + 2 * j];
+        const float2* __restrict__ Ar = p.A + ra * p.a_row;
+        float2 acc[NV];
+#pragma unroll
+        for (int v = 0; v < NV; v++) acc[v] = make_float2(0.f, 0.f);
+#pragma unroll 2
+        for (int kk = tg; kk < K; kk += tpg) {
+            const uint32_t ka = sK[2 * kk], kb = sK[2 * kk + 1];
+            float2 a[NA], b[NB];
+#pragma unroll
+            for (int i = 0; i < NA; i++) a[i] = __ldg(Ar + ka + aoff[i]);
+#pragma unroll
+            for (int j = 0; j < NB; j++) b[j] = sB[kb ^ boff[j]];
+#pragma unroll
+            for (int i = 0; i < NA; i++)
+#pragma unroll
+                for (int j = 0; j < NB; j++) acc[i * NB + j] = cmac(acc[i * NB + j], a[i], b[j]);
+        }
+        // recursive halving over the lanes: after level l the lane keeps half of its values
+        int base = 0;
+#pragma unroll
+        for (int l = 0; l < 5; l++) {
+            const int o = 16 >> l;
+            const int H = NV >> (l + 1);
+            if (H >= 1) {
+                const bool up = (lane & o) != 0;
+#pragma unroll
+                for (int i = 0; i < (NV >> 1); i++) {
+                    if (i < H) {
+                        const float2 lo = acc[i], hi = acc[i + H];
+                        float2 snd = up ? lo : hi;
+                        const float2 keep = up ? hi : lo;
+                        snd.x = __shfl_xor_sync(0xffffffffu, snd.x, o);
+                        snd.y = __shfl_xor_sync(0xffffffffu, snd.y, o);
+                        acc[i] = make_float2(keep.x + snd.x, keep.y + snd.y);
+                    }
+                }
+                if (up) base += H;
+            } else {
+                acc[0].x += __shfl_xor_sync(0xffffffffu, acc[0].x, o);
+                acc[0].y += __shfl_xor_sync(0xffffffffu, acc[0].y, o);
+            }
+        }
+        constexpr int VPL = NV >= 32 ? NV / 32 : 1;  // values per lane after the halving
+        const bool writer = NV >= 32 || (lane & ((32 / NV) - 1)) == 0;
+        if (writer) {
+#pragma unroll
+            for (int i = 0; i < VPL; i++) red[warp * NV + base + i] = acc[i];
+        }
+        __syncthreads();
+        const int wpg = tpg >> 5;
+        for (int t = threadIdx.x; t < (NV << p.g); t += 256) {
+            const int gg = t / NV, o = t % NV;
+            float2 sum = make_float2(0.f, 0.f);
+            for (int u = 0; u < wpg; u++) {
+                const float2 x = red[(gg * wpg + u) * NV + o];
+                sum.x += x.x;
+                sum.y += x.y;
+            }
+            const int ia = (gg << FAT) + o / NB, jb = o % NB;
+            p.C[r * p.c_row + sF[2 * ia + 1] + sF[(2 << p.fa) + 2 * jb + 1]] = sum;
         }
     }
 }
