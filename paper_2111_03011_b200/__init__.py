@@ -211,7 +211,7 @@ class SparseState:
         """tn_bind_device.  workspace: a torch uint8 CUDA tensor (allocated here from torch's caching
         allocator when None, room for `pipelines` concurrent slice pipelines, capped by free memory);
         stream: a torch.cuda.Stream (current stream when None).  The library runs
-        floor(workspace bytes / per-pipeline workspace) slice pipelines concurrently (at most 16)."""
+        floor(workspace bytes / per-pipeline workspace) slice pipelines concurrently (at most 32)."""
         import torch
         if self.info is None:
             raise TnError(TN_EINVAL, "bind before plan")

@@ -207,7 +207,7 @@ tn_status tn_bind_device(tn_ctx* ctx, int device, void* workspace, size_t bytes,
         ctx->dev = nullptr;
     }
     std::string e;
-    int rc = tnb::dev_bind(&ctx->dev, ctx->prog, device, workspace, bytes, cuda_stream, ctx->req.M, 16, e);
+    int rc = tnb::dev_bind(&ctx->dev, ctx->prog, device, workspace, bytes, cuda_stream, ctx->req.M, 32, e);
     if (rc) return fail(ctx, (tn_status)rc, e);
     return TN_OK;
 }

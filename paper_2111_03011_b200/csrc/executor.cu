@@ -94,6 +94,7 @@ struct Launch {
     int64_t gMp = 0, gN2 = 0, gK2 = 0;
     int gEA = 0;
     int gBN = 128;
+    int gCG = 1;  // 2: CTA-pair tiles (cluster of 2, tcgen05 cta_group::2)
     const int4* gTiles = nullptr;
     int gNTiles = 0, gTilesN = 1;
     const int32_t* gPerm = nullptr;
@@ -270,8 +271,96 @@ int set_smem_attrs(std::string& err) {
     CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Cfg<128>::SMEM));
     CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Cfg<64>::SMEM));
     CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Cfg<32>::SMEM));
+    CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            tc::Cfg<128, 2>::SMEM));
+    CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            tc::Cfg<256, 2>::SMEM));
     done = true;
     return TN_OK;
+}
+
+// GEMM tile shape: CTA pairs (256-row tiles, N = 256 when the output is wide) for non-grouped GEMMs with
+// at least 256 D rows and 128 D columns; single-CTA 128 x {128, 64, 32} tiles otherwise.
+void pick_gemm_tile(int64_t Dm, int64_t Dn, bool grouped, int& bn, int& cg) {
+    const char* ev = getenv("TNB_CG");  // TEMP experiment knob: 0 disables CTA pairs
+    const bool pairs = ev ? atoi(ev) != 0 : true;
+    cg = 1;
+    bn = Dn >= 128 ? 128 : (Dn >= 64 ? 64 : 32);
+    if (grouped) {
+        bn = 128;
+        if (pairs && Dm >= 256) {  // the pair table bounds each tile's N to its group (per-tile MMA N)
+            cg = 2;
+            bn = 256;
+        }
+        return;
+    }
+    if (pairs && Dm >= 256 && Dn >= 256) {  // measured: pairs lose at Dn = 128 (config 3 steps 64, 85)
+        cg = 2;
+        bn = 256;
+    }
+}
+
+size_t gemm_smem(int bn, int cg) {
+    if (cg == 2) return bn == 256 ? tc::Cfg<256, 2>::SMEM : tc::Cfg<128, 2>::SMEM;
+    return bn == 128 ? tc::Cfg<128>::SMEM : (bn == 64 ? tc::Cfg<64>::SMEM : tc::Cfg<32>::SMEM);
+}
+
+template <int BN, int CG>
+void launch_gemm_t(const Launch& L, cudaStream_t st) {
+    if constexpr (CG == 1) {
+        tc::k_gemm_tf32x3<BN, 1><<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp,
+                                                                  L.gN2, L.gK2, L.gEA, L.gTiles, L.gPerm, L.gCm, L.gCn,
+                                                                  L.gNTiles, L.gTilesN);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = L.grid;
+        cfg.blockDim = L.block;
+        cfg.dynamicSmemBytes = L.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, tc::k_gemm_tf32x3<BN, 2>, L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp, L.gN2,
+                           L.gK2, L.gEA, L.gTiles, L.gPerm, L.gCm, L.gCn, L.gNTiles, L.gTilesN);
+    }
+}
+
+void launch_gemm(const Launch& L, cudaStream_t st) {
+    if (L.gCG == 2) {
+        if (L.gBN == 256) launch_gemm_t<256, 2>(L, st);
+        else launch_gemm_t<128, 2>(L, st);
+    } else if (L.gBN == 128) {
+        launch_gemm_t<128, 1>(L, st);
+    } else if (L.gBN == 64) {
+        launch_gemm_t<64, 1>(L, st);
+    } else {
+        launch_gemm_t<32, 1>(L, st);
+    }
+}
+
+// fills the GEMM fields of L for D = X Y^T, X [Dm][K2], Y [Dn][K2] (tile shape, tensor maps, grid)
+bool setup_gemm(Launch& L, const void* ahi, const void* alo, const void* bhi, const void* blo, int64_t Dm,
+                int64_t Dn, int64_t K2, bool grouped) {
+    pick_gemm_tile(Dm, Dn, grouped, L.gBN, L.gCG);
+    const int bh = L.gBN / L.gCG;
+    if (!make_map(&L.tm[0], ahi, Dm, K2) || !make_map(&L.tm[1], alo, Dm, K2) || !make_map(&L.tm[2], bhi, Dn, K2, bh) ||
+        !make_map(&L.tm[3], blo, Dn, K2, bh))
+        return false;
+    L.gMp = Dm;
+    L.gK2 = K2;
+    const int64_t bm = (int64_t)tc::BM * L.gCG;
+    const int tiles_m = (int)((Dm + bm - 1) / bm), tiles_n = (int)(Dn / L.gBN);
+    L.gNTiles = tiles_m * tiles_n;
+    // keep the larger operand's tile shared by concurrently running CTAs (read once from HBM)
+    L.gTilesN = (Dn > Dm) ? -tiles_m : tiles_n;
+    L.block = dim3(tc::THREADS);
+    L.smem = gemm_smem(L.gBN, L.gCG);
+    L.grid = dim3((unsigned)(L.gCG * std::min(L.gNTiles, 148 / L.gCG)));  // persistent: one CTA per SM
+    return true;
 }
 
 void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
@@ -295,18 +384,7 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
             kern::k_prep_b<<<L.grid, L.block, L.smem, st>>>(L.pb);
             break;
         case K_GEMM:
-            if (L.gBN == 128)
-                tc::k_gemm_tf32x3<128><<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp,
-                                                                        L.gN2, L.gK2, L.gEA, L.gTiles, L.gPerm, L.gCm,
-                                                                        L.gCn, L.gNTiles, L.gTilesN);
-            else if (L.gBN == 64)
-                tc::k_gemm_tf32x3<64><<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp,
-                                                                       L.gN2, L.gK2, L.gEA, L.gTiles, L.gPerm, L.gCm,
-                                                                       L.gCn, L.gNTiles, L.gTilesN);
-            else
-                tc::k_gemm_tf32x3<32><<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp,
-                                                                       L.gN2, L.gK2, L.gEA, L.gTiles, L.gPerm, L.gCm,
-                                                                       L.gCn, L.gNTiles, L.gTilesN);
+            launch_gemm(L, st);
             break;
         case K_READOUT:
             kern::k_readout<<<L.grid, L.block, 0, st>>>(L.F, L.ridx, P.acc, L.M, P.counter);
@@ -759,33 +837,21 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 const int64_t K2 = 2 * g.k;
                 const int64_t ncols = g.grouped ? g.NB * g.n : g.n;  // complex columns of the prepped B
                 const int64_t Dm = g.embed_a ? 2 * Mp : Mp, Dn = g.embed_a ? ncols : 2 * ncols;
-                // N tile: 128 real columns for wide outputs, 64 / 32 for tall-skinny ones
-                L.gBN = Dn >= 128 ? 128 : (Dn >= 64 ? 64 : 32);
-                if (g.grouped) L.gBN = 128;
-                if (!make_map(&L.tm[0], ptr(g.Ahi), Dm, K2) || !make_map(&L.tm[1], ptr(g.Alo), Dm, K2) ||
-                    !make_map(&L.tm[2], ptr(g.Bhi), Dn, K2, L.gBN) || !make_map(&L.tm[3], ptr(g.Blo), Dn, K2, L.gBN)) {
+                if (!setup_gemm(L, ptr(g.Ahi), ptr(g.Alo), ptr(g.Bhi), ptr(g.Blo), Dm, Dn, K2, g.grouped != 0)) {
                     err = "cuTensorMapEncodeTiled failed";
                     return TN_ECUDA;
                 }
                 L.gC = (float*)ptr(g.C);
-                L.gMp = Dm;
                 L.gN2 = g.embed_a ? g.n : 2 * g.n;
-                L.gK2 = K2;
                 L.gEA = g.embed_a;
-                const int tiles_m = (int)((Dm + tc::BM - 1) / tc::BM), tiles_n = (int)(Dn / L.gBN);
-                L.gNTiles = tiles_m * tiles_n;
-                // keep the larger operand's tile shared by concurrently running CTAs (read once from HBM)
-                L.gTilesN = (Dn > Dm) ? -tiles_m : tiles_n;
                 if (g.grouped) {
-                    L.gTiles = (const int4*)ptr(g.tiles);
+                    L.gTiles = (const int4*)ptr(L.gCG == 2 ? g.tiles2 : g.tiles);
                     L.gPerm = (const int32_t*)ptr(g.perm);
                     L.gCm = g.m;
                     L.gCn = g.n;
-                    L.gNTiles = (int)g.n_tiles;
+                    L.gNTiles = (int)(L.gCG == 2 ? g.n_tiles2 : g.n_tiles);
+                    L.grid = dim3((unsigned)(L.gCG * std::min(L.gNTiles, 148 / L.gCG)));
                 }
-                L.grid = dim3((unsigned)std::min(L.gNTiles, 148));  // persistent: one CTA per SM
-                L.block = dim3(tc::THREADS);
-                L.smem = L.gBN == 128 ? tc::Cfg<128>::SMEM : (L.gBN == 64 ? tc::Cfg<64>::SMEM : tc::Cfg<32>::SMEM);
             }
         } else if (st.kind == K_READOUT) {
             L.F = (const float2*)ptr(st.rp.F);
@@ -833,7 +899,9 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
     std::string skip = getenv("TNB_SKIP") ? std::string(",") + getenv("TNB_SKIP") + "," : std::string();
     for (const Launch& L : P.launches) {
         if (!skip.empty() && (skip.find(",k" + std::to_string(L.kind) + ",") != std::string::npos ||
-                              skip.find(",s" + std::to_string(L.pair) + ",") != std::string::npos))
+                              skip.find(",s" + std::to_string(L.pair) + ",") != std::string::npos ||
+                              skip.find(",x" + std::to_string(L.kind) + "_" + std::to_string(L.pair) + ",") !=
+                                  std::string::npos))
             continue;
         do_launch(d, P, L, P.stream);
     }
@@ -1161,25 +1229,16 @@ int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, i
     pb.b_row = 0;
     pb.log2n = ln;
     kern::k_prep_b<<<grid_for(N * K), 256, (size_t)(pb.ntn + pb.ntk) * 1024, st>>>(pb);
-    CUtensorMap tm[4];
     const int64_t Dm = ea ? 2 * M : M, Dn = ea ? N : 2 * N;
-    const int bn = Dn >= 128 ? 128 : (Dn >= 64 ? 64 : 32);
-    if (!make_map(&tm[0], ahi, Dm, 2 * K) || !make_map(&tm[1], alo, Dm, 2 * K) ||
-        !make_map(&tm[2], bhi, Dn, 2 * K, bn) || !make_map(&tm[3], blo, Dn, 2 * K, bn)) {
+    Launch L;
+    if (!setup_gemm(L, ahi, alo, bhi, blo, Dm, Dn, 2 * K, false)) {
         err = "cuTensorMapEncodeTiled failed";
         return TN_ECUDA;
     }
-    const int tiles_n = (int)(Dn / bn), n_tiles = (int)(((Dm + tc::BM - 1) / tc::BM) * tiles_n);
-    const int g = std::min(n_tiles, 148);
-    if (bn == 128)
-        tc::k_gemm_tf32x3<128><<<g, tc::THREADS, tc::Cfg<128>::SMEM, st>>>(
-            tm[0], tm[1], tm[2], tm[3], C, Dm, ea ? N : 2 * N, 2 * K, ea, nullptr, nullptr, 0, 0, n_tiles, tiles_n);
-    else if (bn == 64)
-        tc::k_gemm_tf32x3<64><<<g, tc::THREADS, tc::Cfg<64>::SMEM, st>>>(
-            tm[0], tm[1], tm[2], tm[3], C, Dm, ea ? N : 2 * N, 2 * K, ea, nullptr, nullptr, 0, 0, n_tiles, tiles_n);
-    else
-        tc::k_gemm_tf32x3<32><<<g, tc::THREADS, tc::Cfg<32>::SMEM, st>>>(
-            tm[0], tm[1], tm[2], tm[3], C, Dm, ea ? N : 2 * N, 2 * K, ea, nullptr, nullptr, 0, 0, n_tiles, tiles_n);
+    L.gC = C;
+    L.gN2 = ea ? N : 2 * N;
+    L.gEA = ea;
+    launch_gemm(L, st);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     cudaFree(ahi);

@@ -17,6 +17,12 @@
 //   warps 2-5       : epilogue, tcgen05.ld 32x32b (TMEM lane quarter = warp % 4) -> registers -> global,
 //                     then arrive on the TMEM-empty barrier.  The accumulator is double-buffered in TMEM
 //                     (2 x 128 columns), so the epilogue of tile i overlaps the MMAs of tile i+1.
+// CTA-pair variant (CG = 2, clusters of 2 CTAs on one TPC): the pair computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2 (M = 256) issued by the leader CTA.  Each CTA TMA-loads its own 128 A rows and
+// half of the B tile (BN/2 rows), completing on the leader's full barrier; the leader's MMA commits are
+// multicast to both CTAs' empty / TMEM-full barriers, and both CTAs' epilogue warps arrive on the leader's
+// TMEM-empty barrier.  Per SM this halves the operand bytes per output at BN = 256 (the GEMMs here are
+// L2->SMEM bandwidth bound); BN = 256 uses one accumulator per TMEM buffer (KSPLIT 1) to fit 512 columns.
 #pragma once
 
 #include <cuda.h>
@@ -34,13 +40,16 @@ constexpr int KSPLIT = 2;       // k-blocks alternate between KSPLIT accumulator
                                 // the tensor-core accumulator truncates, so shorter chains = less bias
 // BN (MMA N = rows of the B tile = real output columns per tile) is a template parameter: 128 for wide
 // contractions, 64 / 32 for tall-skinny ones (long K, few output columns).
-template <int BN>
+template <int BN, int CG = 1>
 struct Cfg {
-    static constexpr int BTILE = BN * BK * 4;                       // B tile bytes
+    static constexpr int BH = BN / CG;                              // B rows (MMA N) held by one CTA
+    static constexpr int BTILE = BH * BK * 4;                       // B tile bytes per CTA
     static constexpr int STAGE = 2 * TILE_BYTES + 2 * BTILE;        // Ahi, Alo, Bhi, Blo
-    static constexpr int STAGES = BN == 128 ? 3 : (BN == 64 ? 4 : 5);
+    static constexpr int STAGES = (200 * 1024) / STAGE < 5 ? (200 * 1024) / STAGE : 5;
     static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
-    static constexpr int TMEM_COLS = 2 * KSPLIT * BN;               // 2 tile buffers x KSPLIT x BN columns
+    static constexpr int KS = BN == 256 ? 1 : KSPLIT;               // accumulators per tile buffer
+    static constexpr int TMEM_COLS = 2 * KS * BN;                   // 2 tile buffers x KS x BN columns
+    static_assert(TMEM_COLS <= 512, "TMEM has 512 columns");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -108,17 +117,67 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
-template <int BN>
+// ---- CTA-pair (cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t map_to_rank(const void* p, uint32_t rank) {  // shared::cluster address
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                              uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {  // arrive on the barrier in both CTAs
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+template <int BN, int CG = 1>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_tf32x3(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                   const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
                   float* __restrict__ C, int64_t Mp, int64_t N2, int64_t K2, int ea,
                   const int4* __restrict__ tiles, const int32_t* __restrict__ perm, int64_t cm, int64_t cn,
                   int n_tiles, int tiles_n) {
-    constexpr int STAGES = Cfg<BN>::STAGES;
-    constexpr int STAGE_BYTES = Cfg<BN>::STAGE;
-    constexpr int TMEM_COLS = Cfg<BN>::TMEM_COLS;
-    constexpr int B0 = 2 * TILE_BYTES, B1 = 2 * TILE_BYTES + Cfg<BN>::BTILE;  // Bhi / Blo offsets
+    using CF = Cfg<BN, CG>;
+    constexpr int STAGES = CF::STAGES;
+    constexpr int STAGE_BYTES = CF::STAGE;
+    constexpr int TMEM_COLS = CF::TMEM_COLS;
+    constexpr int KS = CF::KS;
+    constexpr int BH = CF::BH;
+    constexpr int B0 = 2 * TILE_BYTES, B1 = 2 * TILE_BYTES + CF::BTILE;  // Bhi / Blo offsets
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
@@ -129,6 +188,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nkb = (int)(K2 / BK);
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;       // CTA rank in the pair (0 = MMA leader)
+    const int tile0 = (int)blockIdx.x / CG, tstride = (int)gridDim.x / CG;
     // grouped scatter: cm (rows per output row-block) and cn (columns) are powers of two
     const int lcm = 63 - __clzll(cm > 0 ? cm : 1), lcn = 63 - __clzll(cn > 0 ? cn : 1);
 
@@ -139,18 +200,29 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+            mbar_init(&tempty[b], 4 * CG);  // one arrive per epilogue warp (of both CTAs of a pair)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    if constexpr (CG == 2)
+        cluster_sync_all();  // both CTAs' barriers are initialised before any remote arrive / TMA
+    else
+        __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
@@ -166,29 +238,32 @@ __global__ void __launch_bounds__(THREADS, 1)
             ybase = t1.y;
             goff = t1.z;
         } else if (tiles_n > 0) {  // N fastest: neighbouring CTAs share the A (M-side) tile
-            m0 = (t / tiles_n) * BM;
+            m0 = (t / tiles_n) * BM * CG;
             n0 = (t % tiles_n) * BN;
-            xvalid = BM;
+            xvalid = BM * CG;
             xbase = 0;
             yvalid = BN;
             ybase = 0;
             goff = 0;
         } else {  // tiles_n < 0 encodes M fastest over -tiles_n M-tiles: CTAs share the B tile
-            m0 = (t % (-tiles_n)) * BM;
+            m0 = (t % (-tiles_n)) * BM * CG;
             n0 = (t / (-tiles_n)) * BN;
-            xvalid = BM;
+            xvalid = BM * CG;
             xbase = 0;
             yvalid = BN;
             ybase = 0;
             goff = 0;
         }
+        // this CTA's half of a pair tile: D rows [m0 + rank * BM, +BM)
+        m0 += (int)rank * BM;
+        xvalid -= (int)rank * BM;
     };
 
     if (warp == 0) {
         if (lane == 0) {
             // -------------------------------------------------------- TMA producer
             int it = 0;
-            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            for (int t = tile0; t < n_tiles; t += tstride) {
                 int m0, n0, xv, xb, yv, yb, go;
                 tile_coords(t, m0, n0, xv, xb, yv, yb, go);
                 for (int kb = 0; kb < nkb; kb++, it++) {
@@ -196,28 +271,44 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const uint32_t ph = (it / STAGES) & 1;
                     if (it >= STAGES) mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* st = smem + s * STAGE_BYTES;
-                    mbar_expect_tx(&full[s], STAGE_BYTES);
                     const int kc = kb * BK;
-                    tma_load_2d(st + 0 * TILE_BYTES, &mAhi, &full[s], kc, m0);
-                    tma_load_2d(st + 1 * TILE_BYTES, &mAlo, &full[s], kc, m0);
-                    tma_load_2d(st + B0, &mBhi, &full[s], kc, n0);
-                    tma_load_2d(st + B1, &mBlo, &full[s], kc, n0);
+                    if constexpr (CG == 2) {
+                        // both CTAs' bytes complete on the leader's barrier; the leader arms it for both
+                        const uint32_t fb = map_to_rank(&full[s], 0);
+                        if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+                        // grouped tiles run MMA N = the group's columns (rounded to 16): CTA r holds
+                        // D columns [r * N/2, (r + 1) * N/2) of the tile
+                        const int ntile = tiles ? min(BN, (yv + 15) & ~15) : BN;
+                        const int nb = n0 + (int)rank * (ntile >> 1);
+                        tma_load_2d_pair(st + 0 * TILE_BYTES, &mAhi, fb, kc, m0);
+                        tma_load_2d_pair(st + 1 * TILE_BYTES, &mAlo, fb, kc, m0);
+                        tma_load_2d_pair(st + B0, &mBhi, fb, kc, nb);
+                        tma_load_2d_pair(st + B1, &mBlo, fb, kc, nb);
+                    } else {
+                        mbar_expect_tx(&full[s], STAGE_BYTES);
+                        tma_load_2d(st + 0 * TILE_BYTES, &mAhi, &full[s], kc, m0);
+                        tma_load_2d(st + 1 * TILE_BYTES, &mAlo, &full[s], kc, m0);
+                        tma_load_2d(st + B0, &mBhi, &full[s], kc, n0);
+                        tma_load_2d(st + B1, &mBlo, &full[s], kc, n0);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // -------------------------------------------------------- MMA issuer
-            const uint32_t idesc = idesc_tf32(BM, BN);
+        if (lane == 0 && rank == 0) {
+            // -------------------------------------------------------- MMA issuer (the pair's leader)
             int it = 0, lt = 0;
-            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, lt++) {
+            for (int t = tile0; t < n_tiles; t += tstride, lt++) {
+                int ntile = BN;
+                if (CG == 2 && tiles) ntile = min(BN, (tiles[2 * t + 1].x + 15) & ~15);
+                const uint32_t idesc = idesc_tf32(BM * CG, ntile);
                 const int buf = lt & 1;
                 const uint32_t tph = (lt >> 1) & 1;
                 if (lt >= 2) mbar_wait(&tempty[buf], tph ^ 1);  // epilogue drained this accumulator
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t acc0 = tmem + (uint32_t)(buf * BN * KSPLIT);
+                const uint32_t acc0 = tmem + (uint32_t)(buf * BN * KS);
                 for (int kb = 0; kb < nkb; kb++, it++) {
-                    const uint32_t acc = acc0 + (uint32_t)((kb % KSPLIT) * BN);
+                    const uint32_t acc = acc0 + (uint32_t)((kb % KS) * BN);
                     const int s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(&full[s], ph);
@@ -230,14 +321,27 @@ __global__ void __launch_bounds__(THREADS, 1)
                         const uint64_t dAlo = sdesc_sw128(st + 1 * TILE_BYTES + koff);
                         const uint64_t dBhi = sdesc_sw128(st + B0 + koff);
                         const uint64_t dBlo = sdesc_sw128(st + B1 + koff);
-                        const uint32_t first = (kb < KSPLIT && k == 0) ? 0u : 1u;
-                        mma_tf32(acc, dAlo, dBhi, idesc, first);  // small terms first
-                        mma_tf32(acc, dAhi, dBlo, idesc, 1u);
-                        mma_tf32(acc, dAhi, dBhi, idesc, 1u);
+                        const uint32_t first = (kb < KS && k == 0) ? 0u : 1u;
+                        if constexpr (CG == 2) {
+                            mma_tf32_pair(acc, dAlo, dBhi, idesc, first);  // small terms first
+                            mma_tf32_pair(acc, dAhi, dBlo, idesc, 1u);
+                            mma_tf32_pair(acc, dAhi, dBhi, idesc, 1u);
+                        } else {
+                            mma_tf32(acc, dAlo, dBhi, idesc, first);
+                            mma_tf32(acc, dAhi, dBlo, idesc, 1u);
+                            mma_tf32(acc, dAhi, dBhi, idesc, 1u);
+                        }
                     }
-                    mma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+                    // frees the smem stage (in both CTAs of a pair) once these MMAs have read it
+                    if constexpr (CG == 2)
+                        mma_commit_pair(&empty[s]);
+                    else
+                        mma_commit(&empty[s]);
                 }
-                mma_commit(&tfull[buf]);   // accumulator ready for the epilogue
+                if constexpr (CG == 2)
+                    mma_commit_pair(&tfull[buf]);  // accumulator halves ready for both epilogues
+                else
+                    mma_commit(&tfull[buf]);
             }
         }
     } else {
@@ -245,7 +349,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int quarter = warp & 3;         // TMEM lane quarter this warp may access
         const int row = quarter * 32 + lane;  // TMEM lane = tile row
         int lt = 0;
-        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, lt++) {
+        const uint32_t tempty_leader = CG == 2 ? map_to_rank(&tempty[0], 0) : 0u;
+        for (int t = tile0; t < n_tiles; t += tstride, lt++) {
             int m0, n0, xvalid, xbase, yvalid, ybase, goff;
             tile_coords(t, m0, n0, xvalid, xbase, yvalid, ybase, goff);
             const int buf = lt & 1;
@@ -254,17 +359,18 @@ __global__ void __launch_bounds__(THREADS, 1)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int64_t gm = (int64_t)m0 + row;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
+            const int ncol = (CG == 2 && tiles) ? min(BN, (yvalid + 15) & ~15) : BN;  // MMA N of this tile
+            for (int c0 = 0; c0 < ncol; c0 += 32) {
                 uint32_t v[32];
                 {
                     float f[32];
 #pragma unroll
                     for (int q = 0; q < 32; q++) f[q] = 0.f;
-                    const int nsplit = nkb < KSPLIT ? nkb : KSPLIT;
+                    const int nsplit = nkb < KS ? nkb : KS;
                     for (int sp = 0; sp < nsplit; sp++) {
                         uint32_t u[32];
                         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) +
-                                               (uint32_t)((buf * KSPLIT + sp) * BN + c0);
+                                               (uint32_t)((buf * KS + sp) * BN + c0);
                         asm volatile(
                             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
                             "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -283,7 +389,25 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 if (tiles) {
                     // grouped scatter: D column -> gathered block p = goff + j / cn, fb = j % cn; C row perm[p]
-                    if (!ea) {
+                    if (!ea && cn >= 2) {
+                        // tile columns start group-aligned (cn | 16), so complex pairs (q, q+1) share a block
+                        // and are adjacent in C: one 16-byte store per pair; C has < 2^32 elements (bind)
+                        if (row < xvalid) {
+                            const uint32_t fa = (uint32_t)(m0 - xbase + row);
+                            const uint32_t j0 = (uint32_t)(n0 - ybase + c0) >> 1;
+                            float2* C2 = (float2*)C;
+#pragma unroll
+                            for (int q = 0; q < 16; q += 2) {
+                                if (c0 + 2 * q >= yvalid) break;
+                                const uint32_t j = j0 + (uint32_t)q;
+                                const uint32_t r = (uint32_t)__ldg(perm + goff + (int)(j >> lcn));
+                                const uint32_t idx = ((((r << lcm) + fa) << lcn) + (j & (uint32_t)(cn - 1)));
+                                *(float4*)(C2 + idx) = make_float4(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]),
+                                                                   __uint_as_float(v[2 * q + 2]),
+                                                                   __uint_as_float(v[2 * q + 3]));
+                            }
+                        }
+                    } else if (!ea) {
                         if (row < xvalid) {
                             const int64_t fa = (int64_t)(m0 - xbase) + row;
 #pragma unroll
@@ -357,13 +481,23 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[buf]);
+            if (lane == 0) {
+                if constexpr (CG == 2)
+                    mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * sizeof(uint64_t)));
+                else
+                    mbar_arrive(&tempty[buf]);
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 2) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    if constexpr (CG == 2) {
+        cluster_sync_all();  // neither CTA frees TMEM / exits while its peer's MMAs or arrivals are in flight
+        if (warp == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    } else {
+        __syncthreads();
+        if (warp == 2)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
     }
 }
 

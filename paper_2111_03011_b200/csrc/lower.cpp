@@ -371,31 +371,39 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
                 gp.rowsel = BufRef{REG_MAPS, push_blob(prog.maps, rowsel.data(), rowsel.size() * 4)};
                 gp.embed_a = (RA * m < RC * n) ? 1 : 0;
                 const int xs = gp.embed_a ? 2 : 1, ys = gp.embed_a ? 1 : 2;
-                std::vector<GemmTile> tiles;
-                int64_t q = 0;
-                while (q < RC) {
-                    const int32_t a = ma[perm[q]];
-                    int64_t e = q;
-                    while (e < RC && ma[perm[e]] == a) e++;
-                    const int64_t xb = (int64_t)a * m * xs, xr = m * xs;
-                    const int64_t yb = q * n * ys, yr = (e - q) * n * ys;
-                    for (int64_t x0 = xb; x0 < xb + xr; x0 += 128)
-                        for (int64_t y0 = yb; y0 < yb + yr; y0 += 128) {
-                            GemmTile t;
-                            t.x0 = (int32_t)x0;
-                            t.xvalid = (int32_t)std::min<int64_t>(128, xb + xr - x0);
-                            t.xbase = (int32_t)xb;
-                            t.y0 = (int32_t)y0;
-                            t.yvalid = (int32_t)std::min<int64_t>(128, yb + yr - y0);
-                            t.ybase = (int32_t)yb;
-                            t.off = (int32_t)q;
-                            t.pad = 0;
-                            tiles.push_back(t);
-                        }
-                    q = e;
-                }
-                gp.n_tiles = (int64_t)tiles.size();
-                gp.tiles = BufRef{REG_MAPS, push_blob(prog.maps, tiles.data(), tiles.size() * sizeof(GemmTile))};
+                // tiles never straddle two groups (a tile's A rows are one group's); one table per tile
+                // size: 128 x 128 for single-CTA tiles, 256 x 256 for CTA pairs
+                auto group_tiles = [&](int64_t TX, int64_t TY) {
+                    std::vector<GemmTile> tiles;
+                    int64_t q = 0;
+                    while (q < RC) {
+                        const int32_t a = ma[perm[q]];
+                        int64_t e = q;
+                        while (e < RC && ma[perm[e]] == a) e++;
+                        const int64_t xb = (int64_t)a * m * xs, xr = m * xs;
+                        const int64_t yb = q * n * ys, yr = (e - q) * n * ys;
+                        for (int64_t x0 = xb; x0 < xb + xr; x0 += TX)
+                            for (int64_t y0 = yb; y0 < yb + yr; y0 += TY) {
+                                GemmTile t;
+                                t.x0 = (int32_t)x0;
+                                t.xvalid = (int32_t)std::min<int64_t>(TX, xb + xr - x0);
+                                t.xbase = (int32_t)xb;
+                                t.y0 = (int32_t)y0;
+                                t.yvalid = (int32_t)std::min<int64_t>(TY, yb + yr - y0);
+                                t.ybase = (int32_t)yb;
+                                t.off = (int32_t)q;
+                                t.pad = 0;
+                                tiles.push_back(t);
+                            }
+                        q = e;
+                    }
+                    return tiles;
+                };
+                const std::vector<GemmTile> t1 = group_tiles(128, 128), t2 = group_tiles(256, 256);
+                gp.n_tiles = (int64_t)t1.size();
+                gp.tiles = BufRef{REG_MAPS, push_blob(prog.maps, t1.data(), t1.size() * sizeof(GemmTile))};
+                gp.n_tiles2 = (int64_t)t2.size();
+                gp.tiles2 = BufRef{REG_MAPS, push_blob(prog.maps, t2.data(), t2.size() * sizeof(GemmTile))};
             } else {
                 // embed the smaller operand in the complex-as-real GEMM (its rows double); EA needs n >= 32
                 gp.embed_a = ((Mp < n && n >= 128) || Mp < 128) && n >= 32 ? 1 : 0;

@@ -167,8 +167,10 @@ struct GemmParams {
     int64_t RC = 0;           // output rows (grouped)
     int64_t NB = 0;           // gathered B blocks (= RC)
     int64_t b_row = 0;
-    BufRef perm, rowsel, tiles;
+    BufRef perm, rowsel, tiles;   // tiles: 128 x 128 (single-CTA tiles)
     int64_t n_tiles = 0;
+    BufRef tiles2;                 // 256 x 256 tiles for CTA pairs (same format)
+    int64_t n_tiles2 = 0;
 };
 
 // one output tile of the grouped tensor-core GEMM (D-row / D-col units, see GemmParams::grouped)

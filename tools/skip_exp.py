@@ -12,6 +12,12 @@ info = ss.plan(1 << c.log2_tmax, **c.plan_kwargs())
 ns = 1 << len(info["sliced_wires"])
 pipes = int(os.environ.get("PIPES", "16"))
 variants = sys.argv[1:] or [""]
+if variants == ["each"]:  # every launch of the per-slice graph, skipped one at a time
+    ss.bind(0, pipelines=1)
+    prof = ss.profile_slice(0)
+    kinds = {"instantiate": 0, "apply": 1, "prep_a": 2, "prep_b": 3, "gemm_tcgen05": 4, "readout": 5, "multi": 7}
+    variants = [""] + [f"TNB_SKIP=x{kinds[x['kind']]}_{x['step']}" for x in prof if x["ms"] > 0.015]
+    ms = {f"TNB_SKIP=x{kinds[x['kind']]}_{x['step']}": x["ms"] for x in prof}
 for v in variants:
     for k in ("TNB_SKIP", "TNB_RG"):
         os.environ.pop(k, None)
@@ -24,4 +30,12 @@ for v in variants:
         _, sec = ss.contract(range(ns), timed=True)
         ts.append(sec)
     ts = sorted(ts[2:])
-    print(f"{v!r:28s} {ns / ts[len(ts)//2]:8.1f} slices/s  (min {ns/ts[-1]:.1f} max {ns/ts[0]:.1f})", flush=True)
+    thr = ns / ts[len(ts) // 2]
+    if not v:
+        base = thr
+    extra = ""
+    if v and "base" in globals():
+        extra = f"  marginal {1e3 / base - 1e3 / thr:.4f} ms/slice"
+        if "ms" in globals() and v in ms:
+            extra += f"  (serialized {ms[v]:.4f} ms)"
+    print(f"{v!r:28s} {thr:8.1f} slices/s  (min {ns/ts[-1]:.1f} max {ns/ts[0]:.1f}){extra}", flush=True)
