@@ -307,6 +307,15 @@ def main():
                 "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": dom[0], "peak_src": pk["src"]}
     roof["share_of_slice"] = dom[1]["ms"] / slice_ms
     roof["launches_per_slice"] = dom[1]["launches"]
+    roof["algorithmic_bytes_per_launch"] = dom[1]["bytes"] / max(1, dom[1]["launches"])
+    # traffic: DRAM bytes per launch of this kernel from the committed ncu --set full capture (one slice)
+    tp = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    if os.path.exists(tp):
+        t = json.load(open(tp))
+        if t.get("kernel") == roof["kernel"]:
+            roof["traffic"] = t["dram_bytes_per_launch"]
+            roof["traffic_src"] = t["source"]
+    per_slice_launches, per_contract_launches = ss.launch_counts()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -336,7 +345,7 @@ def main():
             "roofline": roof,
             "kernel_ms_per_slice": {k: round(v["ms"], 4) for k, v in by_kind.items()},
             "clocks": clocks,
-            "gpu_launches": args.steps * (len(block) * launches_per_slice + 1) * (1 if block else 0),
+            "gpu_launches": args.steps * (len(block) * per_slice_launches + per_contract_launches) * (1 if block else 0),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

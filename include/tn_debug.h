@@ -23,6 +23,11 @@ tn_status tn_debug_gemm_tf32x3(const float* A, const float* B, float* C, int64_t
  * (sliceable) edges. */
 tn_status tn_debug_network(const tn_ctx* ctx, int64_t* n_tensors, int64_t* n_edges, int64_t* n_internal);
 
+/* Kernel launches of the bound executor: per_slice = kernels in one slice's graph (after tiny-step fusion);
+ * per_contract = kernels tn_contract issues once (slice-invariant prologue + the final pipeline sum).
+ * A call with n slice ids launches n * per_slice + per_contract kernels.  EINVAL before tn_bind_device. */
+tn_status tn_debug_launch_counts(const tn_ctx* ctx, int64_t* per_slice, int64_t* per_contract);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,7 +66,8 @@ class TnLaunchStat(ctypes.Structure):
 
 
 EXPORTS = ["tn_build", "tn_plan", "tn_plan_dump", "tn_bind_device", "tn_contract", "tn_profile_slice",
-           "tn_sample", "tn_destroy", "tn_last_error", "tn_version", "tn_debug_gemm_tf32x3", "tn_debug_network"]
+           "tn_sample", "tn_destroy", "tn_last_error", "tn_version", "tn_debug_gemm_tf32x3", "tn_debug_network",
+           "tn_debug_launch_counts"]
 
 _lib = None
 
@@ -97,8 +98,9 @@ def lib():
     L.tn_debug_gemm_tf32x3.argtypes = [c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_int64, c.c_int64,
                                        c.c_int32, c.c_void_p]
     L.tn_debug_network.argtypes = [c.c_void_p, P(c.c_int64), P(c.c_int64), P(c.c_int64)]
+    L.tn_debug_launch_counts.argtypes = [c.c_void_p, P(c.c_int64), P(c.c_int64)]
     for name in ("tn_build", "tn_plan", "tn_plan_dump", "tn_bind_device", "tn_contract", "tn_profile_slice",
-                 "tn_sample", "tn_debug_gemm_tf32x3", "tn_debug_network"):
+                 "tn_sample", "tn_debug_gemm_tf32x3", "tn_debug_network", "tn_debug_launch_counts"):
         getattr(L, name).restype = c.c_int
     _lib = L
     return L
@@ -205,6 +207,12 @@ class SparseState:
         a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         self._check(lib().tn_debug_network(self._ctx, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
         return {"tensors": a.value, "edges": b.value, "internal_edges": c.value}
+
+    def launch_counts(self):
+        """(kernels per slice, kernels per tn_contract call) of the bound executor."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        self._check(lib().tn_debug_launch_counts(self._ctx, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
 
     # -------------------------------------------------------------- device
     def bind(self, device: int = 0, workspace=None, stream=None, pipelines: int = 8):

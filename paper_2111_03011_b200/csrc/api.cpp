@@ -319,4 +319,13 @@ tn_status tn_debug_network(const tn_ctx* ctx, int64_t* n_tensors, int64_t* n_edg
     return TN_OK;
 }
 
+tn_status tn_debug_launch_counts(const tn_ctx* ctx, int64_t* per_slice, int64_t* per_contract) {
+    if (!ctx || !ctx->dev) return TN_EINVAL;
+    int64_t a = 0, b = 0;
+    tnb::dev_launch_counts(ctx->dev, &a, &b);
+    if (per_slice) *per_slice = a;
+    if (per_contract) *per_contract = b;
+    return TN_OK;
+}
+
 }  // extern "C"

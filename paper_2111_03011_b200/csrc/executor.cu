@@ -89,6 +89,7 @@ struct Launch {
     kern::RowGemmDev rgp;
     kern::PrepADev pa;
     kern::PrepBDev pb;
+    kern::PrepTDev pt;  // K_PREP_A / K_PREP_B run the tiled pre-pass k_prep_t
     CUtensorMap tm[4];
     float* gC = nullptr;
     int64_t gMp = 0, gN2 = 0, gK2 = 0;
@@ -106,13 +107,11 @@ struct Launch {
     const float2* F = nullptr;
     const int64_t* ridx = nullptr;
     int64_t M = 0;
-    // operand extents in bytes (apply), for the megakernel's hazard analysis
+    // operand extents in bytes (apply), for the tiny-step chains' hazard analysis
     int64_t a_bytes = 0, b_bytes = 0, c_bytes = 0;
-    // multi (small-step megakernel)
+    // K_MULTI: a k_chain run of tiny steps
     size_t m_first = 0;          // index into Device::msteps_host
     int m_n = 0;
-    int64_t m_items = 0;
-    size_t m_sync = 0;           // int offset into Device::sync
 };
 
 }  // namespace
@@ -134,7 +133,6 @@ struct Pipe {
     std::vector<Launch> launches;
     std::vector<kern::MStep> msteps_host;
     kern::MStep* msteps = nullptr;
-    int* sync = nullptr;
 };
 
 struct Device {
@@ -266,8 +264,6 @@ int set_smem_attrs(std::string& err) {
 #undef SETR
     CK(set_rg_attrs_fb<0>()); CK(set_rg_attrs_fb<1>()); CK(set_rg_attrs_fb<2>());
     CK(set_rg_attrs_fb<3>()); CK(set_rg_attrs_fb<4>()); CK(set_rg_attrs_fb<5>());
-    CK(cudaFuncSetAttribute(kern::k_prep_a, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    CK(cudaFuncSetAttribute(kern::k_prep_b, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Cfg<128>::SMEM));
     CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Cfg<64>::SMEM));
     CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Cfg<32>::SMEM));
@@ -279,22 +275,20 @@ int set_smem_attrs(std::string& err) {
     return TN_OK;
 }
 
-// GEMM tile shape: CTA pairs (256-row tiles, N = 256 when the output is wide) for non-grouped GEMMs with
-// at least 256 D rows and 128 D columns; single-CTA 128 x {128, 64, 32} tiles otherwise.
+// GEMM tile shape: CTA pairs (256 x 256 tiles) when D has at least 256 rows and, for plain GEMMs, 256
+// columns (grouped tiles bound N per tile); single-CTA 128 x {128, 64, 32} tiles otherwise.
 void pick_gemm_tile(int64_t Dm, int64_t Dn, bool grouped, int& bn, int& cg) {
-    const char* ev = getenv("TNB_CG");  // TEMP experiment knob: 0 disables CTA pairs
-    const bool pairs = ev ? atoi(ev) != 0 : true;
     cg = 1;
     bn = Dn >= 128 ? 128 : (Dn >= 64 ? 64 : 32);
     if (grouped) {
         bn = 128;
-        if (pairs && Dm >= 256) {  // the pair table bounds each tile's N to its group (per-tile MMA N)
+        if (Dm >= 256) {  // the pair table bounds each tile's N to its group (per-tile MMA N)
             cg = 2;
             bn = 256;
         }
         return;
     }
-    if (pairs && Dm >= 256 && Dn >= 256) {  // measured: pairs lose at Dn = 128 (config 3 steps 64, 85)
+    if (Dm >= 256 && Dn >= 256) {  // measured: pairs lose at Dn = 128 (config 3 steps 64, 85)
         cg = 2;
         bn = 256;
     }
@@ -378,10 +372,8 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
             else launch_apply_ni<1>(L, st);
             break;
         case K_PREP_A:
-            kern::k_prep_a<<<L.grid, L.block, L.smem, st>>>(L.pa);
-            break;
         case K_PREP_B:
-            kern::k_prep_b<<<L.grid, L.block, L.smem, st>>>(L.pb);
+            kern::k_prep_t<<<L.grid, L.block, 0, st>>>(L.pt);
             break;
         case K_GEMM:
             launch_gemm(L, st);
@@ -390,16 +382,19 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
             kern::k_readout<<<L.grid, L.block, 0, st>>>(L.F, L.ridx, P.acc, L.M, P.counter);
             break;
         case K_MULTI:
-            cudaMemsetAsync(P.sync + L.m_sync, 0, (size_t)(L.m_n + 1) * sizeof(int), st);
-            kern::k_multi<<<L.grid, L.block, 0, st>>>(P.msteps + L.m_first, L.m_n, L.m_items, P.sync + L.m_sync);
+            kern::k_chain<<<1, 256, 0, st>>>(P.msteps + L.m_first, L.m_n);
             break;
     }
 }
 
-// Fuse runs of consecutive small K_APPLY launches into K_MULTI launches (see kern::k_multi).
+// Fuse runs of consecutive tiny K_APPLY launches into K_MULTI launches (kern::k_chain).
 std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
-    auto small = [](const Launch& L) {
-        return L.kind == K_APPLY && L.ap.ktab != nullptr && L.ap.R * L.ap.n_orbits <= 65536 && L.cmac <= 4.0e6 &&
+    // tiny steps (<= 256 work items: one per thread of one CTA) are fused into k_chain runs; larger ones
+    // keep their own multi-CTA launch (measured: fusing up to 65536 items in a multi-CTA ticket kernel, or
+    // chaining up to 8192 in one CTA, were both slower on config 3)
+    constexpr int64_t fuse_max = 256;
+    auto small = [&](const Launch& L) {
+        return L.kind == K_APPLY && L.ap.ktab != nullptr && L.ap.R * L.ap.n_orbits <= fuse_max && L.cmac <= 4.0e6 &&
                !L.ap.stage_b && !L.rows_mode && !L.na && !L.rg;
     };
     auto ov = [](const void* a, int64_t na, const void* b, int64_t nb) {
@@ -409,7 +404,6 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
     };
     std::vector<Launch> out;
     size_t i = 0;
-    size_t sync_off = 0;
     while (i < in.size()) {
         if (!small(in[i])) {
             out.push_back(in[i++]);
@@ -417,8 +411,7 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
         }
         size_t j = i;
         std::vector<kern::MStep> run;
-        int64_t items = 0;
-        while (j < in.size() && small(in[j]) && run.size() < 1024) {
+        while (j < in.size() && small(in[j]) && run.size() < (size_t)kern::CHAIN_MAX_STEPS) {
             const Launch& L = in[j];
             kern::MStep m;
             std::memset(&m, 0, sizeof(m));
@@ -441,8 +434,6 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
                 m.inner_c[t] = L.ap.inner_c[t];
                 m.inner_b[t] = L.ap.inner_b[t];
             }
-            m.chunks = (int)((m.total + 255) / 256);
-            m.item_begin = items;
             // hazards against earlier steps of the run
             std::vector<int> deps;
             for (int t = 0; t < (int)run.size(); t++) {
@@ -466,7 +457,6 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
             if ((int)red.size() > kern::MULTI_MAX_DEPS) break;
             m.ndep = (int)red.size();
             for (int k = 0; k < m.ndep; k++) m.dep[k] = red[k];
-            items += m.chunks;
             run.push_back(m);
             j++;
         }
@@ -484,13 +474,21 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
         }
         M.m_first = P.msteps_host.size();
         M.m_n = (int)run.size();
-        M.m_items = items;
-        M.m_sync = sync_off;
-        sync_off += run.size() + 1;
         M.rows = (int64_t)run.size();
         M.block = dim3(256);
-        static const int multi_grid = getenv("TNB_MULTI_GRID") ? atoi(getenv("TNB_MULTI_GRID")) : 296;
-        M.grid = dim3((unsigned)std::min<int64_t>(items, multi_grid));
+        // one CTA runs the chain in program order (k_chain); a barrier goes before a step that depends on
+        // one issued since the previous barrier
+        {
+            M.grid = dim3(1);
+            int open_from = 0;
+            for (int t = 0; t < (int)run.size(); t++) {
+                bool bar = false;
+                for (int k = 0; k < run[t].ndep; k++)
+                    if (run[t].dep[k] >= open_from) bar = true;
+                run[t].barrier = bar ? 1 : 0;
+                if (bar) open_from = t;
+            }
+        }
         P.msteps_host.insert(P.msteps_host.end(), run.begin(), run.end());
         out.push_back(M);
         i = j;
@@ -507,6 +505,76 @@ dim3 grid_for(int64_t threads, int64_t per_block = 256, int64_t cap = 148 * 16) 
 }  // namespace
 
 namespace {
+
+// Tables of the tiled pre-pass k_prep_t for output-index bit b <- source bit pi[b] (b < lin): the tile S is
+// the output's 5 lowest bits, the bits that land on the source's 5 lowest bits, then the next-lowest output
+// bits up to 10; the remaining ("outer") bits index tiles through byte tables.  Appends to `tabs` (16-B
+// aligned blocks) and returns the offsets.
+struct PrepTTabs {
+    size_t tin = 0, tout = 0, outer = 0;
+    int n_tile = 0, nto = 0;
+};
+
+PrepTTabs prep_t_tables(std::vector<uint32_t>& tabs, const std::vector<int>& pi) {
+    const int lin = (int)pi.size();
+    std::vector<bool> in_s(lin, false);
+    for (int b = 0; b < lin; b++)
+        if (b < 5 || pi[b] < 5) in_s[b] = true;
+    int cnt = 0;
+    for (int b = 0; b < lin; b++) cnt += in_s[b];
+    for (int b = 0; b < lin && cnt < std::min(lin, 10); b++)
+        if (!in_s[b]) {
+            in_s[b] = true;
+            cnt++;
+        }
+    std::vector<int> s_out, outer;
+    for (int b = 0; b < lin; b++) (in_s[b] ? s_out : outer).push_back(b);
+    std::vector<int> s_src = s_out;
+    std::sort(s_src.begin(), s_src.end(), [&](int x, int y) { return pi[x] < pi[y]; });
+    std::vector<int> slot_of(lin, -1);
+    for (int j = 0; j < (int)s_out.size(); j++) slot_of[s_out[j]] = j;
+    PrepTTabs t;
+    t.n_tile = (int)s_out.size();
+    const int tn = 1 << t.n_tile;
+    auto align = [&]() { tabs.resize((tabs.size() + 3) & ~(size_t)3, 0); };
+    align();
+    t.tin = tabs.size();
+    for (int e = 0; e < tn; e++) {
+        uint32_t slot = 0, so = 0;
+        for (int j = 0; j < t.n_tile; j++)
+            if ((e >> j) & 1) {
+                slot |= 1u << slot_of[s_src[j]];
+                so |= 1u << pi[s_src[j]];
+            }
+        tabs.push_back(slot);
+        tabs.push_back(so);
+    }
+    align();
+    t.tout = tabs.size();
+    for (int e = 0; e < tn; e++) {
+        uint32_t oo = 0;
+        for (int j = 0; j < t.n_tile; j++)
+            if ((e >> j) & 1) oo |= 1u << s_out[j];
+        tabs.push_back(oo);
+    }
+    align();
+    t.outer = tabs.size();
+    t.nto = ((int)outer.size() + 7) / 8;
+    for (int q = 0; q < t.nto; q++)
+        for (int v = 0; v < 256; v++) {
+            uint32_t so = 0, oo = 0;
+            for (int b = 0; b < 8; b++) {
+                const int j = 8 * q + b;
+                if (j < (int)outer.size() && ((v >> b) & 1)) {
+                    so |= 1u << pi[outer[j]];
+                    oo |= 1u << outer[j];
+                }
+            }
+            tabs.push_back(so);
+            tabs.push_back(oo);
+        }
+    return t;
+}
 
 // Resolve the step program into launches for pipeline P (workspace base P.work), fuse small steps,
 // upload its tables and capture its per-slice graph.
@@ -671,13 +739,11 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
             }
             // row GEMM: long k, few outputs per row, B's row small enough to stage (k_apply_rg)
             {
-                const char* ev = getenv("TNB_RG");  // TEMP experiment knob: 0 off, 1 default, 2 over rows mode
-                const int rgm = ev ? atoi(ev) : 1;
                 const int fa = a.cA.n, fb = a.cB.n;
                 const int FB = fb, FAT = std::min(fa, 5 - FB), g = fa - FAT;
-                if (rgm && fa + fb == a.dC && a.nk >= 6 && a.nk <= kern::KTAB_MAX_BITS && FB <= 5 && FAT >= 0 &&
+                if (fa + fb == a.dC && a.nk >= 6 && a.nk <= kern::KTAB_MAX_BITS && FB <= 5 && FAT >= 0 &&
                     FAT + FB >= 1 && g <= 3 && a.R >= 64 && a.b_row >= 16 && a.b_row <= 8192 &&
-                    a.a_row >= a.b_row && st.cmac > 4.0e6 && !L.na && (rgm == 2 || !L.rows_mode)) {
+                    a.a_row >= a.b_row && st.cmac > 4.0e6 && !L.na && !L.rows_mode) {
                     L.rg = 1;
                     L.rows_mode = 0;
                     L.team = 1;
@@ -794,16 +860,28 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 std::vector<int> mm(lm), kk(lk);
                 for (int t = 0; t < lm; t++) mm[g.aM.dst[t]] = g.aM.src[t];
                 for (int t = 0; t < lk; t++) kk[g.aK.dst[t]] = g.aK.src[t];
-                tabs.resize((tabs.size() + 3) & ~(size_t)3, 0);
-            size_t base = tabs.size();
-                std::vector<uint32_t> t1((size_t)p.ntm * 256, 0), t2((size_t)p.ntk * 256, 0);
-                if (p.ntm) push_tables(t1, mm, 1, 0);
-                if (p.ntk) push_tables(t2, kk, 1, 0);
-                tabs.insert(tabs.end(), t1.begin(), t1.end());
-                tabs.insert(tabs.end(), t2.begin(), t2.end());
-                fixes.push_back({P.launches.size(), 2, base});
-                L.smem = (size_t)(p.ntm + p.ntk) * 256 * 4;
-                L.grid = grid_for(Mp * g.k, 256, 148 * 16);
+                // output index bits: k bits lowest, then m bits
+                std::vector<int> pi(kk);
+                pi.insert(pi.end(), mm.begin(), mm.end());
+                const PrepTTabs tt = prep_t_tables(tabs, pi);
+                kern::PrepTDev& q = L.pt;
+                std::memset(&q, 0, sizeof(q));
+                q.src = p.A;
+                q.rowmap = p.ma;
+                q.hi = p.hi;
+                q.lo = p.lo;
+                q.R = g.R;
+                q.src_row = g.a_row;
+                q.log2_row = lm + lk;
+                q.log2k = lk;
+                q.n_tile = tt.n_tile;
+                q.nto = tt.nto;
+                q.embed = g.embed_a;
+                fixes.push_back({P.launches.size(), 6, tt.tin});
+                fixes.push_back({P.launches.size(), 7, tt.tout});
+                fixes.push_back({P.launches.size(), 8, tt.outer});
+                L.smem = 0;
+                L.grid = dim3((unsigned)std::min<int64_t>(g.R << (lm + lk - tt.n_tile), 148 * 16));
             } else if (st.kind == K_PREP_B) {
                 kern::PrepBDev& p = L.pb;
                 p.B = (const float2*)ptr(g.B);
@@ -822,16 +900,27 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 std::vector<int> nn(ln), kk(lk);
                 for (int t = 0; t < ln; t++) nn[g.bN.dst[t]] = g.bN.src[t];
                 for (int t = 0; t < lk; t++) kk[g.bK.dst[t]] = g.bK.src[t];
-                tabs.resize((tabs.size() + 3) & ~(size_t)3, 0);
-            size_t base = tabs.size();
-                std::vector<uint32_t> t1((size_t)p.ntn * 256, 0), t2((size_t)p.ntk * 256, 0);
-                if (p.ntn) push_tables(t1, nn, 1, 0);
-                if (p.ntk) push_tables(t2, kk, 1, 0);
-                tabs.insert(tabs.end(), t1.begin(), t1.end());
-                tabs.insert(tabs.end(), t2.begin(), t2.end());
-                fixes.push_back({P.launches.size(), 3, base});
-                L.smem = (size_t)(p.ntn + p.ntk) * 256 * 4;
-                L.grid = grid_for(p.N * g.k, 256, 148 * 16);
+                std::vector<int> pi(kk);
+                pi.insert(pi.end(), nn.begin(), nn.end());
+                const PrepTTabs tt = prep_t_tables(tabs, pi);
+                kern::PrepTDev& q = L.pt;
+                std::memset(&q, 0, sizeof(q));
+                q.src = p.B;
+                q.rowmap = p.rowsel;
+                q.hi = p.hi;
+                q.lo = p.lo;
+                q.R = g.grouped ? g.NB : 1;
+                q.src_row = g.grouped ? g.b_row : 0;
+                q.log2_row = ln + lk;
+                q.log2k = lk;
+                q.n_tile = tt.n_tile;
+                q.nto = tt.nto;
+                q.embed = p.embed;
+                fixes.push_back({P.launches.size(), 6, tt.tin});
+                fixes.push_back({P.launches.size(), 7, tt.tout});
+                fixes.push_back({P.launches.size(), 8, tt.outer});
+                L.smem = 0;
+                L.grid = dim3((unsigned)std::min<int64_t>(q.R << (ln + lk - tt.n_tile), 148 * 16));
             } else {
                 // D = X Y^T with X [Dm][2K], Y [Dn][2K] (see gemm_tc.cuh)
                 const int64_t K2 = 2 * g.k;
@@ -873,7 +962,10 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
         else if (f.which == 2) L.pa.tab = p;
         else if (f.which == 3) L.pb.tab = p;
         else if (f.which == 4) L.rgp.ktab = p;
-        else L.rgp.ftab = p;
+        else if (f.which == 5) L.rgp.ftab = p;
+        else if (f.which == 6) L.pt.tin = (const uint2*)p;
+        else if (f.which == 7) L.pt.tout = p;
+        else L.pt.outer = (const uint2*)p;
     }
 
     P.launches = fuse_small(P, P.launches);
@@ -881,10 +973,6 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
         CK(cudaMalloc(&P.msteps, P.msteps_host.size() * sizeof(kern::MStep)));
         CK(cudaMemcpy(P.msteps, P.msteps_host.data(), P.msteps_host.size() * sizeof(kern::MStep),
                       cudaMemcpyHostToDevice));
-        size_t nsync = 0;
-        for (const Launch& L : P.launches)
-            if (L.kind == K_MULTI) nsync = std::max(nsync, L.m_sync + L.m_n + 1);
-        CK(cudaMalloc(&P.sync, nsync * sizeof(int)));
     }
     CK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&P.done, cudaEventDisableTiming));
@@ -895,7 +983,9 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
     CK(cudaMemset(P.slice_ids, 0, P.slice_cap * sizeof(uint64_t)));
     CK(cudaMemset(P.counter, 0, sizeof(int64_t)));
     CK(cudaStreamBeginCapture(P.stream, cudaStreamCaptureModeThreadLocal));
-    // TEMP experiment knob: TNB_SKIP="k2,k3,s56" drops launches of kind 2, 3 and of step 56 from the graph
+    // diagnostics only (tools/skip_exp.py): TNB_SKIP="k2,s56,x4_102" leaves launches of kind 2, of step 56 and
+    // the kind-4 launch of step 102 out of the captured graph, to measure each launch's marginal throughput
+    // cost under concurrent pipelines.  The amplitudes are then wrong; never set it otherwise.
     std::string skip = getenv("TNB_SKIP") ? std::string(",") + getenv("TNB_SKIP") + "," : std::string();
     for (const Launch& L : P.launches) {
         if (!skip.empty() && (skip.find(",k" + std::to_string(L.kind) + ",") != std::string::npos ||
@@ -1127,6 +1217,11 @@ int dev_profile(Device* d, uint64_t slice_id, tn_launch_stat* stats, int max_sta
 
 int dev_pipes(const Device* d) { return d ? (int)d->pipes.size() : 0; }
 
+void dev_launch_counts(const Device* d, int64_t* per_slice, int64_t* per_contract) {
+    *per_slice = d->pipes.empty() ? 0 : (int64_t)d->pipes[0].launches.size();
+    *per_contract = (d->has_pre ? (int64_t)d->pre.launches.size() : 0) + 1;  // + k_finalize / k_sum_pipes
+}
+
 void dev_destroy(Device* d) {
     if (!d) return;
     cudaSetDevice(d->dev);
@@ -1140,7 +1235,6 @@ void dev_destroy(Device* d) {
         cudaFree(P.counter);
         cudaFree(P.slice_ids);
         cudaFree(P.msteps);
-        cudaFree(P.sync);
         if (P.done) cudaEventDestroy(P.done);
         if (P.stream) cudaStreamDestroy(P.stream);
     }
@@ -1179,56 +1273,48 @@ int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, i
     int lk = 0, ln = 0;
     while ((1ll << lk) < K) lk++;
     while ((1ll << ln) < N) ln++;
-    // A: m index bits -> A bits (row-major [M][K]: m bit b -> bit b + lk), k bits -> bits 0..lk-1.
-    // Use R = M rows of m = 1 so that ragged M works: A row stride = K.
+    // pre-passes through k_prep_t, as in the pipeline.  A [M][K] row-major: M rows of m = 1, output k bit t
+    // <- A bit t.  B [K][N] row-major: output (n, k), k bit t <- B bit ln + t, n bit t <- B bit t.
     std::vector<uint32_t> tab;
-    std::vector<int> kk(lk), nn(ln), kb(lk);
-    for (int t = 0; t < lk; t++) kk[t] = t;
-    std::vector<uint32_t> tk((size_t)((lk + 7) / 8) * 256, 0);
-    push_tables(tk, kk, 1, 0);
-    // B[k][n]: k bit t -> bit t + ln, n bit t -> bit t
-    for (int t = 0; t < ln; t++) nn[t] = t;
-    for (int t = 0; t < lk; t++) kb[t] = t + ln;
-    std::vector<uint32_t> tn((size_t)((ln + 7) / 8) * 256, 0), tkb((size_t)((lk + 7) / 8) * 256, 0);
-    push_tables(tn, nn, 1, 0);
-    push_tables(tkb, kb, 1, 0);
-    tab.insert(tab.end(), tk.begin(), tk.end());
-    size_t off_b = tab.size();
-    tab.insert(tab.end(), tn.begin(), tn.end());
-    tab.insert(tab.end(), tkb.begin(), tkb.end());
+    std::vector<int> pa_pi(lk), pb_pi;
+    for (int t = 0; t < lk; t++) pa_pi[t] = t;
+    for (int t = 0; t < lk; t++) pb_pi.push_back(ln + t);
+    for (int t = 0; t < ln; t++) pb_pi.push_back(t);
+    const PrepTTabs ta = prep_t_tables(tab, pa_pi), tb = prep_t_tables(tab, pb_pi);
     uint32_t* dtab;
     CK(cudaMalloc(&dtab, tab.size() * 4));
     CK(cudaMemcpy(dtab, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
-    kern::PrepADev pa;
-    pa.A = (const float2*)A;
-    pa.ma = nullptr;
-    pa.hi = (float2*)ahi;
-    pa.lo = (float2*)alo;
-    pa.Mp = M;
-    pa.K = K;
-    pa.a_row = K;
-    pa.log2m = 0;
-    pa.log2k = lk;
-    pa.tab = dtab;
-    pa.ntm = 0;
-    pa.ntk = (lk + 7) / 8;
-    pa.embed = ea;
-    kern::k_prep_a<<<grid_for(M * K), 256, (size_t)pa.ntk * 1024, st>>>(pa);
-    kern::PrepBDev pb;
-    pb.B = (const float2*)B;
-    pb.hi = (float2*)bhi;
-    pb.lo = (float2*)blo;
-    pb.N = N;
-    pb.K = K;
-    pb.log2k = lk;
-    pb.tab = dtab + off_b;
-    pb.ntn = (ln + 7) / 8;
-    pb.ntk = (lk + 7) / 8;
-    pb.embed = !ea;
-    pb.rowsel = nullptr;
-    pb.b_row = 0;
-    pb.log2n = ln;
-    kern::k_prep_b<<<grid_for(N * K), 256, (size_t)(pb.ntn + pb.ntk) * 1024, st>>>(pb);
+    kern::PrepTDev qa;
+    std::memset(&qa, 0, sizeof(qa));
+    qa.src = (const float2*)A;
+    qa.hi = (float2*)ahi;
+    qa.lo = (float2*)alo;
+    qa.R = M;
+    qa.src_row = K;
+    qa.log2_row = lk;
+    qa.log2k = lk;
+    qa.n_tile = ta.n_tile;
+    qa.nto = ta.nto;
+    qa.tin = (const uint2*)(dtab + ta.tin);
+    qa.tout = dtab + ta.tout;
+    qa.outer = (const uint2*)(dtab + ta.outer);
+    qa.embed = ea;
+    kern::k_prep_t<<<(unsigned)std::min<int64_t>(M << (lk - ta.n_tile), 148 * 16), 256, 0, st>>>(qa);
+    kern::PrepTDev qb;
+    std::memset(&qb, 0, sizeof(qb));
+    qb.src = (const float2*)B;
+    qb.hi = (float2*)bhi;
+    qb.lo = (float2*)blo;
+    qb.R = 1;
+    qb.log2_row = ln + lk;
+    qb.log2k = lk;
+    qb.n_tile = tb.n_tile;
+    qb.nto = tb.nto;
+    qb.tin = (const uint2*)(dtab + tb.tin);
+    qb.tout = dtab + tb.tout;
+    qb.outer = (const uint2*)(dtab + tb.outer);
+    qb.embed = !ea;
+    kern::k_prep_t<<<(unsigned)std::min<int64_t>((int64_t)1 << (ln + lk - tb.n_tile), 148 * 16), 256, 0, st>>>(qb);
     const int64_t Dm = ea ? 2 * M : M, Dn = ea ? N : 2 * N;
     Launch L;
     if (!setup_gemm(L, ahi, alo, bhi, blo, Dm, Dn, 2 * K, false)) {

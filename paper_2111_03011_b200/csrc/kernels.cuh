@@ -313,91 +313,78 @@ __global__ void __launch_bounds__(256) k_apply_rows(const ApplyDev p) {
     }
 }
 
-// ---------------------------------------------------------------------------- small-step megakernel
-// A run of consecutive small contraction steps executed by ONE persistent launch.  Work items are
-// (step, chunk of 256 orbits) in program order; a block takes the next ticket, waits until the steps
-// it depends on (RAW / WAR / WAW on workspace buffers) have all their chunks done, computes one orbit
-// per thread, and publishes its chunk.  A block only waits on tickets already taken by running blocks,
-// so the scheme cannot deadlock.  Operands are read with ld.global.cg (L2) because the workspace is
-// reused within the run.
+// ---------------------------------------------------------------------------- tiny-step chains
+// A run of consecutive tiny contraction steps (<= 256 work items each: leaf cones absorbing gates one at a
+// time) executed by ONE CTA in program order.  Dependencies (RAW / WAR / WAW on workspace buffers) become
+// __syncthreads before the dependent step; operands are read with ld.global.cg (L2) and written with
+// st.global.cg because the run reuses workspace buffers.
 constexpr int MULTI_MAX_DEPS = 8;
+constexpr int CHAIN_MAX_STEPS = 64;    // steps per k_chain launch (descriptors staged in smem)
 struct MStep {
     const float2* A;
     const float2* B;
     float2* C;
     const int32_t* ma;
     const int32_t* mb;
-    int64_t a_row, b_row, c_row, n_orbits, total, item_begin;
+    int64_t a_row, b_row, c_row, n_orbits, total;
     const uint32_t* tab;
     const uint32_t* ktab;
-    int ntab, nk, ni, ndep, chunks, pad;
+    int ntab, nk, ni, ndep, barrier, pad;  // barrier: k_chain syncs the CTA before this step
     int dep[MULTI_MAX_DEPS];
     uint32_t inner_c[16], inner_b[16];
 };
 
-__global__ void __launch_bounds__(256) k_multi(const MStep* __restrict__ steps, int nsteps, int64_t n_items,
-                                               int* __restrict__ sync) {
-    int* ticket = sync;
-    int* done = sync + 1;
-    __shared__ int s_item, s_step;
-    while (true) {
-        if (threadIdx.x == 0) {
-            const int it = atomicAdd(ticket, 1);
-            s_item = it;
-            if (it < n_items) {
-                int s = 0;
-                while (s + 1 < nsteps && steps[s + 1].item_begin <= it) s++;
-                s_step = s;
-                const MStep& S = steps[s];
-                for (int d = 0; d < S.ndep; d++) {
-                    const int dd = S.dep[d];
-                    const int need = steps[dd].chunks;
-                    while (atomicAdd(&done[dd], 0) < need) __nanosleep(64);
-                }
-                __threadfence();
-            }
-        }
-        __syncthreads();
-        const int it = s_item;
-        if (it >= n_items) break;
-        const MStep& S = steps[s_step];
-        const int64_t w = (int64_t)(it - S.item_begin) * 256 + threadIdx.x;
-        if (w < S.total) {
-            const int64_t r = w / S.n_orbits;
-            const int64_t o = w - r * S.n_orbits;
-            uint32_t coff = 0, aoff = 0, boff = 0;
-            for (int t = 0; t < S.ntab; t++) {
-                const uint4 e = __ldg(((const uint4*)S.tab) + (t << 8) + (int)((o >> (8 * t)) & 255));
-                coff += e.x;
-                aoff += e.y;
-                boff += e.z;
-            }
-            const int64_t ra = S.ma ? (int64_t)__ldg(S.ma + r) : r;
-            const int64_t rb = S.mb ? (int64_t)__ldg(S.mb + r) : 0;
-            const float2* Ar = S.A + ra * S.a_row + aoff;
-            const float2* Br = S.B + rb * S.b_row + boff;
-            const int nout = 1 << S.ni;
-            const int64_t K = (int64_t)1 << S.nk;
-            float2 acc[16];
+// one work item (output orbit w) of a fused tiny step
+__device__ __forceinline__ void multi_item(const MStep& S, int64_t w) {
+    const int64_t r = w / S.n_orbits;
+    const int64_t o = w - r * S.n_orbits;
+    uint32_t coff = 0, aoff = 0, boff = 0;
+    for (int t = 0; t < S.ntab; t++) {
+        const uint4 e = __ldg(((const uint4*)S.tab) + (t << 8) + (int)((o >> (8 * t)) & 255));
+        coff += e.x;
+        aoff += e.y;
+        boff += e.z;
+    }
+    const int64_t ra = S.ma ? (int64_t)__ldg(S.ma + r) : r;
+    const int64_t rb = S.mb ? (int64_t)__ldg(S.mb + r) : 0;
+    const float2* Ar = S.A + ra * S.a_row + aoff;
+    const float2* Br = S.B + rb * S.b_row + boff;
+    const int nout = 1 << S.ni;
+    const int64_t K = (int64_t)1 << S.nk;
+    float2 acc[16];
 #pragma unroll
-            for (int ii = 0; ii < 16; ii++) acc[ii] = make_float2(0.f, 0.f);
-            for (int64_t kk = 0; kk < K; kk++) {
-                const uint2 kab = __ldg(((const uint2*)S.ktab) + kk);
-                const float2 a = __ldcg(Ar + kab.x);
+    for (int ii = 0; ii < 16; ii++) acc[ii] = make_float2(0.f, 0.f);
+#pragma unroll 4
+    for (int64_t kk = 0; kk < K; kk++) {
+        const uint2 kab = __ldg(((const uint2*)S.ktab) + kk);
+        const float2 a = __ldcg(Ar + kab.x);
 #pragma unroll
-                for (int ii = 0; ii < 16; ii++)
-                    if (ii < nout) acc[ii] = cmac(acc[ii], a, __ldcg(Br + kab.y + S.inner_b[ii]));
-            }
-            float2* Cr = S.C + r * S.c_row + coff;
+        for (int ii = 0; ii < 16; ii++)
+            if (ii < nout) acc[ii] = cmac(acc[ii], a, __ldcg(Br + kab.y + S.inner_b[ii]));
+    }
+    float2* Cr = S.C + r * S.c_row + coff;
 #pragma unroll
-            for (int ii = 0; ii < 16; ii++)
-                if (ii < nout) __stcg(Cr + S.inner_c[ii], acc[ii]);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(&done[s_step], 1);
-        }
+    for (int ii = 0; ii < 16; ii++)
+        if (ii < nout) __stcg(Cr + S.inner_c[ii], acc[ii]);
+}
+
+// a __syncthreads only before a step that depends on a step issued since the previous barrier (S.barrier,
+// host-computed from the run's hazards), so independent neighbours overlap.
+__global__ void __launch_bounds__(256) k_chain(const MStep* __restrict__ steps, int nsteps) {
+    // the run's descriptors live in smem: the item loop reads table pointers / offsets with LDS, not with a
+    // chain of dependent global loads per output
+    __shared__ MStep sS[CHAIN_MAX_STEPS];
+    {
+        const int words = nsteps * (int)(sizeof(MStep) / 4);
+        const uint32_t* src = (const uint32_t*)steps;
+        uint32_t* dst = (uint32_t*)sS;
+        for (int i = threadIdx.x; i < words; i += 256) dst[i] = src[i];
+    }
+    __syncthreads();
+    for (int s = 0; s < nsteps; s++) {
+        const MStep& S = sS[s];
+        if (S.barrier) __syncthreads();
+        for (int64_t w = threadIdx.x; w < S.total; w += 256) multi_item(S, w);
     }
 }
 
@@ -545,38 +532,6 @@ struct PrepADev {
     int embed;
 };
 
-__global__ void __launch_bounds__(256) k_prep_a(const PrepADev p) {
-    extern __shared__ uint32_t sm[];
-    const int tn = (p.ntm + p.ntk) * 256;
-    for (int i = threadIdx.x; i < tn; i += blockDim.x) sm[i] = p.tab[i];
-    __syncthreads();
-    const int64_t total = p.Mp * p.K;
-    const int64_t mmask = ((int64_t)1 << p.log2m) - 1;
-    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total; it += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t mp = it >> p.log2k;
-        const int64_t kk = it & (p.K - 1);
-        const int64_t r = mp >> p.log2m;
-        const int64_t mi = mp & mmask;
-        uint32_t off = 0;
-        for (int t = 0; t < p.ntm; t++) off += sm[(t << 8) + (int)((mi >> (8 * t)) & 255)];
-        for (int t = 0; t < p.ntk; t++) off += sm[((p.ntm + t) << 8) + (int)((kk >> (8 * t)) & 255)];
-        const int64_t ra = p.ma ? (int64_t)p.ma[r] : r;
-        const float2 v = p.A[ra * p.a_row + off];
-        const float2 h = make_float2(tf32_hi(v.x), tf32_hi(v.y));
-        const float2 l = make_float2(v.x - h.x, v.y - h.y);
-        if (!p.embed) {
-            p.hi[it] = h;
-            p.lo[it] = l;
-        } else {  // rows 2m = (ar, -ai), 2m+1 = (ai, ar) along K
-            const int64_t i0 = (2 * mp) * p.K + kk, i1 = (2 * mp + 1) * p.K + kk;
-            p.hi[i0] = make_float2(h.x, -h.y);
-            p.lo[i0] = make_float2(l.x, -l.y);
-            p.hi[i1] = make_float2(h.y, h.x);
-            p.lo[i1] = make_float2(l.y, l.x);
-        }
-    }
-}
-
 struct PrepBDev {
     const float2* B;
     float2* hi;   // [2N][K] float2 = [2N][2K] fp32 (embedded) or [N][K] float2 (plain)
@@ -591,33 +546,68 @@ struct PrepBDev {
     int log2n;
 };
 
-__global__ void __launch_bounds__(256) k_prep_b(const PrepBDev p) {
-    extern __shared__ uint32_t sm[];
-    const int tn = (p.ntn + p.ntk) * 256;
-    for (int i = threadIdx.x; i < tn; i += blockDim.x) sm[i] = p.tab[i];
-    __syncthreads();
-    const int64_t total = p.N * p.K;
-    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total; it += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t nn = it >> p.log2k;
-        const int64_t kk = it & (p.K - 1);
-        const int64_t fbi = p.rowsel ? (nn & (((int64_t)1 << p.log2n) - 1)) : nn;
-        uint32_t off = 0;
-        for (int t = 0; t < p.ntn; t++) off += sm[(t << 8) + (int)((fbi >> (8 * t)) & 255)];
-        for (int t = 0; t < p.ntk; t++) off += sm[((p.ntn + t) << 8) + (int)((kk >> (8 * t)) & 255)];
-        const int64_t rb = p.rowsel ? (int64_t)p.rowsel[nn >> p.log2n] : 0;
-        const float2 b = p.B[rb * p.b_row + off];
-        const float hr = tf32_hi(b.x), hi_ = tf32_hi(b.y);
-        const float lr = b.x - hr, li = b.y - hi_;
-        if (!p.embed) {
-            p.hi[it] = make_float2(hr, hi_);
-            p.lo[it] = make_float2(lr, li);
-            continue;
+// Tiled pre-pass (both GEMM operands): out[r][x][k] (K-major, hi/lo split, optionally embedded) =
+// src[rowmap(r)][pi(x, k)] for a bit permutation pi.  One CTA per tile: the tile spans the source's and the
+// output's lowest bits (<= 2^10 elements), read coalesced from the source into a swizzled smem tile,
+// written coalesced in output order.  Embedding (the operand on the embedded side of the complex-as-real
+// GEMM): rows 2x = (re, -im), 2x+1 = (im, re) along K.
+struct PrepTDev {
+    const float2* src;
+    const int32_t* rowmap;   // source row of output row r (null: r)
+    float2* hi;
+    float2* lo;
+    int64_t R, src_row;      // output rows, source row stride (elements)
+    int log2_row, log2k;     // output bits per row (x and k bits), k bits
+    int n_tile;              // tile bits |S|
+    const uint2* tin;        // [2^n_tile]: (smem slot, source offset), source order
+    const uint32_t* tout;    // [2^n_tile]: output offset, output order (slot = index)
+    const uint2* outer;      // [nto][256]: outer index byte -> (source offset, output offset)
+    int nto;
+    int embed;
+};
+
+__device__ __forceinline__ int prep_swz(int slot) { return slot ^ (((slot >> 4) ^ (slot >> 8)) & 15); }
+
+__global__ void __launch_bounds__(256) k_prep_t(const PrepTDev p) {
+    __shared__ float2 tile[1024];
+    const int tn = 1 << p.n_tile;
+    const int64_t n_outer = (int64_t)1 << (p.log2_row - p.n_tile);
+    const int64_t K = (int64_t)1 << p.log2k;
+    for (int64_t blk = blockIdx.x; blk < p.R * n_outer; blk += gridDim.x) {
+        const int64_t r = blk >> (p.log2_row - p.n_tile);
+        const int64_t o = blk & (n_outer - 1);
+        uint32_t so = 0, oo = 0;
+        for (int t = 0; t < p.nto; t++) {
+            const uint2 e = __ldg(p.outer + (t << 8) + (int)((o >> (8 * t)) & 255));
+            so += e.x;
+            oo += e.y;
         }
-        // Bt row 2nn = (br, -bi), row 2nn+1 = (bi, br) along K (complex-as-real embedding)
-        p.hi[(2 * nn) * p.K + kk] = make_float2(hr, -hi_);
-        p.lo[(2 * nn) * p.K + kk] = make_float2(lr, -li);
-        p.hi[(2 * nn + 1) * p.K + kk] = make_float2(hi_, hr);
-        p.lo[(2 * nn + 1) * p.K + kk] = make_float2(li, lr);
+        const int64_t sr = p.rowmap ? (int64_t)__ldg(p.rowmap + r) : r;
+        const float2* __restrict__ src = p.src + sr * p.src_row + so;
+        for (int e = threadIdx.x; e < tn; e += 256) {
+            const uint2 t = __ldg(p.tin + e);
+            tile[prep_swz((int)t.x)] = __ldg(src + t.y);
+        }
+        __syncthreads();
+        const int64_t obase = (r << p.log2_row) + oo;
+        for (int e = threadIdx.x; e < tn; e += 256) {
+            const float2 v = tile[prep_swz(e)];
+            const int64_t it = obase + __ldg(p.tout + e);
+            const float2 h = make_float2(tf32_hi(v.x), tf32_hi(v.y));
+            const float2 l = make_float2(v.x - h.x, v.y - h.y);
+            if (!p.embed) {
+                p.hi[it] = h;
+                p.lo[it] = l;
+            } else {
+                const int64_t x = it >> p.log2k, kk = it & (K - 1);
+                const int64_t i0 = (2 * x) * K + kk, i1 = i0 + K;
+                p.hi[i0] = make_float2(h.x, -h.y);
+                p.lo[i0] = make_float2(l.x, -l.y);
+                p.hi[i1] = make_float2(h.y, h.x);
+                p.lo[i1] = make_float2(l.y, l.x);
+            }
+        }
+        __syncthreads();
     }
 }
 

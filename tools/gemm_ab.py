@@ -15,4 +15,9 @@ for v in sys.argv[1:]:
         p = ss.profile_slice(0)
     rows = [x for x in p if x["kind"] == "gemm_tcgen05"]
     tot = sum(x["ms"] for x in rows)
+    kinds = {}
+    for x in p:
+        kinds[x["kind"]] = kinds.get(x["kind"], 0.0) + x["ms"]
     print(f"{v:12s} gemm total {tot:.4f} ms: " + " ".join(f"s{x['step']}:{x['ms']:.4f}" for x in rows), flush=True)
+    print("    kinds: " + " ".join(f"{k}:{t:.3f}" for k, t in sorted(kinds.items(), key=lambda kv: -kv[1])) +
+          f"  total {sum(kinds.values()):.3f} ms in {len(p)} launches", flush=True)
