@@ -109,6 +109,7 @@ struct Launch {
     int64_t M = 0;
     // operand extents in bytes (apply), for the tiny-step chains' hazard analysis
     int64_t a_bytes = 0, b_bytes = 0, c_bytes = 0;
+    std::vector<MemAcc> mem;     // workspace / persistent ranges read and written (graph dependencies)
     // K_MULTI: a k_chain run of tiny steps
     size_t m_first = 0;          // index into Device::msteps_host
     int m_n = 0;
@@ -151,7 +152,10 @@ struct Device {
     std::vector<Pipe> pipes;
     int64_t M = 0;
     int s = 0;
+    std::vector<cudaStream_t> capture_streams;  // fork streams used while capturing the graphs (DAG)
 };
+
+constexpr int kCaptureStreams = 4;  // + the pipeline's own stream
 
 namespace {
 
@@ -471,6 +475,7 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
         for (size_t t = i; t < j; t++) {
             M.cmac += in[t].cmac;
             M.bytes += in[t].bytes;
+            M.mem.insert(M.mem.end(), in[t].mem.begin(), in[t].mem.end());
         }
         M.m_first = P.msteps_host.size();
         M.m_n = (int)run.size();
@@ -597,6 +602,7 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
         L.pair = st.pair;
         L.cmac = st.cmac;
         L.bytes = st.bytes;
+        L.mem = st.mem;
         L.block = dim3(256);
         if (st.kind == K_INSTANTIATE) {
             L.itab = (const InstLeafDesc*)ptr(st.ip.table);
@@ -982,20 +988,86 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
     CK(cudaMalloc(&P.slice_ids, P.slice_cap * sizeof(uint64_t)));
     CK(cudaMemset(P.slice_ids, 0, P.slice_cap * sizeof(uint64_t)));
     CK(cudaMemset(P.counter, 0, sizeof(int64_t)));
-    CK(cudaStreamBeginCapture(P.stream, cudaStreamCaptureModeThreadLocal));
     // diagnostics only (tools/skip_exp.py): TNB_SKIP="k2,s56,x4_102" leaves launches of kind 2, of step 56 and
     // the kind-4 launch of step 102 out of the captured graph, to measure each launch's marginal throughput
     // cost under concurrent pipelines.  The amplitudes are then wrong; never set it otherwise.
     std::string skip = getenv("TNB_SKIP") ? std::string(",") + getenv("TNB_SKIP") + "," : std::string();
-    for (const Launch& L : P.launches) {
+    std::vector<int> keep;
+    for (int i = 0; i < (int)P.launches.size(); i++) {
+        const Launch& L = P.launches[i];
         if (!skip.empty() && (skip.find(",k" + std::to_string(L.kind) + ",") != std::string::npos ||
                               skip.find(",s" + std::to_string(L.pair) + ",") != std::string::npos ||
                               skip.find(",x" + std::to_string(L.kind) + "_" + std::to_string(L.pair) + ",") !=
                                   std::string::npos))
             continue;
-        do_launch(d, P, L, P.stream);
+        keep.push_back(i);
     }
+    // The graph is a DAG: launch i depends on every earlier launch whose workspace / persistent ranges
+    // conflict with its own (RAW, WAR, WAW).  Captured on a small stream pool: a launch goes to the stream
+    // whose last launch is one of its dependencies (else to an idle stream) and waits on events for the
+    // others, so independent branches (leaf cones, the stem) run concurrently within a slice.
+    auto conflict = [](const Launch& a, const Launch& b) {
+        for (const MemAcc& x : a.mem)
+            for (const MemAcc& y : b.mem)
+                if (x.region == y.region && (x.write || y.write) && x.offset < y.offset + y.bytes &&
+                    y.offset < x.offset + x.bytes)
+                    return true;
+        return false;
+    };
+    const int nl = (int)keep.size();
+    std::vector<std::vector<int>> deps(nl);
+    for (int a = 0; a < nl; a++)
+        for (int b = 0; b < a; b++)
+            if (conflict(P.launches[keep[a]], P.launches[keep[b]])) deps[a].push_back(b);
+    std::vector<cudaStream_t>& pool = d->capture_streams;
+    while (pool.size() < (size_t)kCaptureStreams) {
+        cudaStream_t x;
+        CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+        pool.push_back(x);
+    }
+    std::vector<cudaEvent_t> ev(nl + 1 + kCaptureStreams);
+    for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaStreamBeginCapture(P.stream, cudaStreamCaptureModeThreadLocal));
+    CK(cudaEventRecord(ev[nl], P.stream));  // fork point
+    std::vector<cudaStream_t> ss = {P.stream};
+    ss.insert(ss.end(), pool.begin(), pool.end());
+    std::vector<int> tail(ss.size(), -1), on(nl, -1);
+    std::vector<bool> forked(ss.size(), false);
+    forked[0] = true;
+    for (int a = 0; a < nl; a++) {
+        int sel = -1;
+        for (int b : deps[a])  // a stream whose last launch is a dependency (the latest one)
+            for (size_t q = 0; q < ss.size(); q++)
+                if (tail[q] == b && (sel < 0 || tail[sel] < b)) sel = (int)q;
+        if (sel < 0)
+            for (size_t q = 0; q < ss.size(); q++)
+                if (tail[q] < 0) {  // an unused stream
+                    sel = (int)q;
+                    break;
+                }
+        if (sel < 0) {  // all busy: the stream whose last launch is oldest
+            sel = 0;
+            for (size_t q = 1; q < ss.size(); q++)
+                if (tail[q] < tail[sel]) sel = (int)q;
+        }
+        if (!forked[sel]) {
+            CK(cudaStreamWaitEvent(ss[sel], ev[nl], 0));
+            forked[sel] = true;
+        }
+        for (int b : deps[a])
+            if (on[b] != sel) CK(cudaStreamWaitEvent(ss[sel], ev[b], 0));
+        do_launch(d, P, P.launches[keep[a]], ss[sel]);
+        CK(cudaEventRecord(ev[a], ss[sel]));
+        tail[sel] = a;
+        on[a] = sel;
+    }
+    for (size_t q = 1; q < ss.size(); q++)  // join
+        if (forked[q]) {
+            CK(cudaEventRecord(ev[nl + q], ss[q]));
+            CK(cudaStreamWaitEvent(P.stream, ev[nl + q], 0));
+        }
     cudaError_t ce = cudaStreamEndCapture(P.stream, &P.graph);
+    for (auto& e : ev) cudaEventDestroy(e);
     if (ce != cudaSuccess) {
         err = std::string("graph capture failed: ") + cudaGetErrorString(ce);
         return TN_ECUDA;
@@ -1247,6 +1319,7 @@ void dev_destroy(Device* d) {
     if (d->ev0) cudaEventDestroy(d->ev0);
     if (d->ev1) cudaEventDestroy(d->ev1);
     if (d->evu) cudaEventDestroy(d->evu);
+    for (cudaStream_t x : d->capture_streams) cudaStreamDestroy(x);
     delete d;
 }
 

@@ -104,6 +104,16 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     for (int i = 0; i < s; i++) js << (i ? "," : "") << wire_str(net, plan.sliced[i]);
     js << "],\"leaves\":[";
 
+    auto acc = [](Step& st, const BufRef& b, int64_t bytes, bool write) {
+        if (b.region != REG_WORK && b.region != REG_PERS) return;
+        MemAcc m;
+        m.region = b.region;
+        m.write = write ? 1 : 0;
+        m.offset = b.offset;
+        m.bytes = bytes;
+        st.mem.push_back(m);
+    };
+
     // ---------------------------------------------------------------- leaves: bank + instantiation
     std::vector<InstLeafDesc> inst;
     int64_t inst_items = 0;
@@ -160,6 +170,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         st.ip.n_leaves = (int32_t)inst.size();
         st.ip.table = BufRef{REG_MAPS, push_blob(prog.maps, inst.data(), inst.size() * sizeof(InstLeafDesc))};
         st.bytes = 16.0 * inst_items;
+        for (const InstLeafDesc& d : inst) acc(st, BufRef{REG_WORK, d.out_off}, d.items * 8, true);
         prog.steps.push_back(st);
     }
 
@@ -292,6 +303,9 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             ap.C = Cn.buf;
             ap.a_elems = sizeA;
             ap.b_elems = sizeB;
+            acc(st, A->buf, sizeA * 8, false);
+            acc(st, B->buf, sizeB * 8, false);
+            acc(st, Cn.buf, Cn.bytes, true);
             st.cmac = cmac;
             st.bytes = 8.0 * (double)(sizeA + sizeB + RC * ap.c_row) + (maRef.region ? 4.0 * RC : 0) + (mbRef.region ? 4.0 * RC : 0);
             {
@@ -433,6 +447,17 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             sg.gp = gp;
             sg.cmac = cmac;
             sg.bytes = 2.0 * abytes + 2.0 * bbytes + 8.0 * RC * m * n;
+            acc(sa, A->buf, sizeA * 8, false);
+            acc(sa, gp.Ahi, abytes, true);
+            acc(sa, gp.Alo, abytes, true);
+            acc(sb, B->buf, sizeB * 8, false);
+            acc(sb, gp.Bhi, bbytes, true);
+            acc(sb, gp.Blo, bbytes, true);
+            acc(sg, gp.Ahi, abytes, false);
+            acc(sg, gp.Alo, abytes, false);
+            acc(sg, gp.Bhi, bbytes, false);
+            acc(sg, gp.Blo, bbytes, false);
+            acc(sg, Cn.buf, Cn.bytes, true);
             out.push_back(sa);
             out.push_back(sb);
             out.push_back(sg);
@@ -493,6 +518,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     st.rp.M = req.M;
     st.rp.idx = BufRef{REG_MAPS, push_blob(prog.maps, idx.data(), idx.size() * 8)};
     st.bytes = (8.0 + 8.0 + 32.0) * (double)req.M;
+    acc(st, F.buf, ((int64_t)F.rows.size() << dF) * 8, false);
     prog.steps.push_back(st);
 
     js << "],\"final\":{\"qmask\":" << F.qmask << ",\"rows\":" << F.rows.size() << ",\"legs\":[";

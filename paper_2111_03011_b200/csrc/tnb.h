@@ -190,10 +190,19 @@ struct ReadoutParams {
     int64_t M = 0;
 };
 
+// one workspace / persistent-region range a step reads or writes (the executor derives the graph's
+// dependency edges from these: RAW / WAR / WAW overlaps)
+struct MemAcc {
+    int32_t region = REG_NONE;
+    int32_t write = 0;
+    int64_t offset = 0, bytes = 0;
+};
+
 struct Step {
     int32_t kind = 0;
     int32_t pair = -1;        // pairwise step index
     double cmac = 0, bytes = 0;
+    std::vector<MemAcc> mem;  // REG_WORK / REG_PERS accesses (bank and maps are read-only)
     ApplyParams ap;
     GemmParams gp;
     InstParams ip;
