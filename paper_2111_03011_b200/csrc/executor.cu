@@ -518,6 +518,7 @@ namespace {
 struct PrepTTabs {
     size_t tin = 0, tout = 0, outer = 0;
     int n_tile = 0, nto = 0;
+    int pairs = 0;  // 1: 16-byte loads / stores of element pairs (tile has >= 2 elements)
 };
 
 PrepTTabs prep_t_tables(std::vector<uint32_t>& tabs, const std::vector<int>& pi) {
@@ -540,6 +541,10 @@ PrepTTabs prep_t_tables(std::vector<uint32_t>& tabs, const std::vector<int>& pi)
     for (int j = 0; j < (int)s_out.size(); j++) slot_of[s_out[j]] = j;
     PrepTTabs t;
     t.n_tile = (int)s_out.size();
+    // load pairs (e, e+1) in source order differ in source bit 0 and store pairs in output order in output
+    // bit 0 (both always tile bits), so 16-byte accesses work once the tile has 2 elements; the caller also
+    // needs K >= 2 so that an embedded pair stays inside one row
+    t.pairs = t.n_tile >= 1 ? 1 : 0;
     const int tn = 1 << t.n_tile;
     auto align = [&]() { tabs.resize((tabs.size() + 3) & ~(size_t)3, 0); };
     align();
@@ -882,6 +887,7 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 q.log2k = lk;
                 q.n_tile = tt.n_tile;
                 q.nto = tt.nto;
+                q.pairs = tt.pairs && lk >= 1;
                 q.embed = g.embed_a;
                 fixes.push_back({P.launches.size(), 6, tt.tin});
                 fixes.push_back({P.launches.size(), 7, tt.tout});
@@ -921,6 +927,7 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 q.log2k = lk;
                 q.n_tile = tt.n_tile;
                 q.nto = tt.nto;
+                q.pairs = tt.pairs && lk >= 1;
                 q.embed = p.embed;
                 fixes.push_back({P.launches.size(), 6, tt.tin});
                 fixes.push_back({P.launches.size(), 7, tt.tout});
@@ -1372,6 +1379,7 @@ int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, i
     qa.tout = dtab + ta.tout;
     qa.outer = (const uint2*)(dtab + ta.outer);
     qa.embed = ea;
+    qa.pairs = ta.pairs && lk >= 1;
     kern::k_prep_t<<<(unsigned)std::min<int64_t>(M << (lk - ta.n_tile), 148 * 16), 256, 0, st>>>(qa);
     kern::PrepTDev qb;
     std::memset(&qb, 0, sizeof(qb));
@@ -1387,6 +1395,7 @@ int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, i
     qb.tout = dtab + tb.tout;
     qb.outer = (const uint2*)(dtab + tb.outer);
     qb.embed = !ea;
+    qb.pairs = tb.pairs && lk >= 1;
     kern::k_prep_t<<<(unsigned)std::min<int64_t>((int64_t)1 << (ln + lk - tb.n_tile), 148 * 16), 256, 0, st>>>(qb);
     const int64_t Dm = ea ? 2 * M : M, Dn = ea ? N : 2 * N;
     Launch L;

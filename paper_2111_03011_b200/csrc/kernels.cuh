@@ -564,6 +564,7 @@ struct PrepTDev {
     const uint2* outer;      // [nto][256]: outer index byte -> (source offset, output offset)
     int nto;
     int embed;
+    int pairs;               // 16-byte loads / stores of element pairs (tile >= 2 elements, K >= 2)
 };
 
 __device__ __forceinline__ int prep_swz(int slot) { return slot ^ (((slot >> 4) ^ (slot >> 8)) & 15); }
@@ -584,27 +585,59 @@ __global__ void __launch_bounds__(256) k_prep_t(const PrepTDev p) {
         }
         const int64_t sr = p.rowmap ? (int64_t)__ldg(p.rowmap + r) : r;
         const float2* __restrict__ src = p.src + sr * p.src_row + so;
-        for (int e = threadIdx.x; e < tn; e += 256) {
-            const uint2 t = __ldg(p.tin + e);
-            tile[prep_swz((int)t.x)] = __ldg(src + t.y);
+        if (p.pairs) {
+            // source-order pairs (2e, 2e+1) differ in source bit 0, output-order pairs in output bit 0:
+            // 16-byte loads and stores
+            for (int e = 2 * threadIdx.x; e < tn; e += 512) {
+                const uint2 t = __ldg(p.tin + e);
+                const float4 v = __ldg((const float4*)(src + t.y));
+                const uint2 t1 = __ldg(p.tin + e + 1);
+                tile[prep_swz((int)t.x)] = make_float2(v.x, v.y);
+                tile[prep_swz((int)t1.x)] = make_float2(v.z, v.w);
+            }
+        } else {
+            for (int e = threadIdx.x; e < tn; e += 256) {
+                const uint2 t = __ldg(p.tin + e);
+                tile[prep_swz((int)t.x)] = __ldg(src + t.y);
+            }
         }
         __syncthreads();
         const int64_t obase = (r << p.log2_row) + oo;
-        for (int e = threadIdx.x; e < tn; e += 256) {
-            const float2 v = tile[prep_swz(e)];
-            const int64_t it = obase + __ldg(p.tout + e);
-            const float2 h = make_float2(tf32_hi(v.x), tf32_hi(v.y));
-            const float2 l = make_float2(v.x - h.x, v.y - h.y);
-            if (!p.embed) {
-                p.hi[it] = h;
-                p.lo[it] = l;
-            } else {
-                const int64_t x = it >> p.log2k, kk = it & (K - 1);
-                const int64_t i0 = (2 * x) * K + kk, i1 = i0 + K;
-                p.hi[i0] = make_float2(h.x, -h.y);
-                p.lo[i0] = make_float2(l.x, -l.y);
-                p.hi[i1] = make_float2(h.y, h.x);
-                p.lo[i1] = make_float2(l.y, l.x);
+        if (p.pairs) {
+            for (int e = 2 * threadIdx.x; e < tn; e += 512) {
+                const float2 v0 = tile[prep_swz(e)], v1 = tile[prep_swz(e + 1)];
+                const int64_t it = obase + __ldg(p.tout + e);
+                const float4 h = make_float4(tf32_hi(v0.x), tf32_hi(v0.y), tf32_hi(v1.x), tf32_hi(v1.y));
+                const float4 l = make_float4(v0.x - h.x, v0.y - h.y, v1.x - h.z, v1.y - h.w);
+                if (!p.embed) {
+                    *(float4*)(p.hi + it) = h;
+                    *(float4*)(p.lo + it) = l;
+                } else {
+                    const int64_t x = it >> p.log2k, kk = it & (K - 1);
+                    const int64_t i0 = (2 * x) * K + kk, i1 = i0 + K;
+                    *(float4*)(p.hi + i0) = make_float4(h.x, -h.y, h.z, -h.w);
+                    *(float4*)(p.lo + i0) = make_float4(l.x, -l.y, l.z, -l.w);
+                    *(float4*)(p.hi + i1) = make_float4(h.y, h.x, h.w, h.z);
+                    *(float4*)(p.lo + i1) = make_float4(l.y, l.x, l.w, l.z);
+                }
+            }
+        } else {
+            for (int e = threadIdx.x; e < tn; e += 256) {
+                const float2 v = tile[prep_swz(e)];
+                const int64_t it = obase + __ldg(p.tout + e);
+                const float2 h = make_float2(tf32_hi(v.x), tf32_hi(v.y));
+                const float2 l = make_float2(v.x - h.x, v.y - h.y);
+                if (!p.embed) {
+                    p.hi[it] = h;
+                    p.lo[it] = l;
+                } else {
+                    const int64_t x = it >> p.log2k, kk = it & (K - 1);
+                    const int64_t i0 = (2 * x) * K + kk, i1 = i0 + K;
+                    p.hi[i0] = make_float2(h.x, -h.y);
+                    p.lo[i0] = make_float2(l.x, -l.y);
+                    p.hi[i1] = make_float2(h.y, h.x);
+                    p.lo[i1] = make_float2(l.y, l.x);
+                }
             }
         }
         __syncthreads();

@@ -356,6 +356,16 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             const bool a_low = low_is_K(A) && (grouped || !maRef.region);
             const bool b_low = low_is_K(B);
             gemm_json = std::string(",\"a_lowK\":") + (a_low ? "1" : "0") + ",\"b_lowK\":" + (b_low ? "1" : "0");
+            {
+                auto ids = [](const std::vector<int>& v) {
+                    std::string o = "[";
+                    for (size_t t = 0; t < v.size(); t++) o += (t ? "," : "") + std::to_string(v[t]);
+                    return o + "]";
+                };
+                // leg ids (MSB first) of both operands, the contracted legs and the free legs, in GEMM order
+                gemm_json += ",\"legs_a\":" + ids(A->legs) + ",\"legs_b\":" + ids(B->legs) + ",\"legs_k\":" +
+                             ids(K) + ",\"legs_fa\":" + ids(fa) + ",\"legs_fb\":" + ids(fb);
+            }
             gp.aK.n = (int)K.size();
             gp.bK.n = (int)K.size();
             for (int t = 0; t < gp.aK.n; t++) {
