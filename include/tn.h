@@ -166,6 +166,33 @@ tn_status tn_profile_slice(tn_ctx* ctx, uint64_t slice_id, tn_launch_stat* stats
 tn_status tn_sample(const tn_ctx* ctx, const float* amps, const float* ideal_amps, int64_t n_slices_summed,
                     uint64_t seed, uint64_t* samples_out, double est[3]);
 
+/* tn_sample_report -- host.  The sampler with a choice of within-group method plus the validation
+ * estimators of the paper's supplement.
+ *   sampler 0: the categorical draw of tn_sample (frugal within a group).
+ *   sampler 1: uniform-proposal Metropolis chain over the group's l indices ("a Markov chain ...
+ *              using the Metropolis algorithm"): splitmix64 stream keyed by
+ *              (seed, TAG 5), words c = g*(2*steps+1) + t, u_c = top 53 bits * 2^-53; start
+ *              x = floor(u_c0 * l); step t proposes y = floor(u_{c0+2t-1} * l) and moves when
+ *              u_{c0+2t} * w(x) < w(y), w = |a|^2 in fp64; the sample is the state after `steps` steps
+ *              (only the final state is returned, so a burn-in is implicit).  steps >= 1.
+ *   index_out (nullable): L indices j into the M requested bitstrings (samples_out[g] = bits[j]).
+ *   rep: the estimators below; phat_j = |a_j|^2 / F_norm is the approximate distribution normalised by
+ *   the paper's estimate F_norm = (2^n/M) sum |a|^2.  Fields that need ideal_amps are NaN
+ *   without them; a zero probability yields +-inf.
+ * EINVAL on bad arguments; ENUMERIC on an all-zero group. */
+typedef struct {
+    double f;                /* n_slices_summed / 2^s                                          */
+    double F_norm;           /* (2^n/M) sum_j |a_j|^2                                     */
+    double xeb;              /* (2^n/L) sum_i P(s_i) - 1, P = |ideal|^2                    */
+    double log_xeb;          /* <ln(2^n P(s_i))> + Euler's gamma ("logarithmic XEB")     */
+    double entropy_samples;  /* -<ln phat(s_i)> over the L samples                      */
+    double entropy_state;    /* -(2^n/M) sum_j phat_j ln phat_j: the sparse state's distribution        */
+    double pt_ks;            /* KS distance of {2^n phat_j} to Exp(1) (Porter-Thomas)          */
+} tn_report;
+tn_status tn_sample_report(const tn_ctx* ctx, const float* amps, const float* ideal_amps, int64_t n_slices_summed,
+                           uint64_t seed, int32_t sampler, int32_t steps, uint64_t* samples_out, int64_t* index_out,
+                           tn_report* rep);
+
 void tn_destroy(tn_ctx* ctx);
 const char* tn_last_error(const tn_ctx* ctx);
 const char* tn_version(void);

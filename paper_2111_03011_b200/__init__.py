@@ -65,9 +65,14 @@ class TnLaunchStat(ctypes.Structure):
                 ("n", ctypes.c_int64), ("k", ctypes.c_int64), ("rows", ctypes.c_int64)]
 
 
+class TnReport(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_double) for name in
+                ("f", "F_norm", "xeb", "log_xeb", "entropy_samples", "entropy_state", "pt_ks")]
+
+
 EXPORTS = ["tn_build", "tn_plan", "tn_plan_dump", "tn_bind_device", "tn_contract", "tn_profile_slice",
-           "tn_sample", "tn_destroy", "tn_last_error", "tn_version", "tn_debug_gemm_tf32x3", "tn_debug_network",
-           "tn_debug_launch_counts"]
+           "tn_sample", "tn_sample_report", "tn_destroy", "tn_last_error", "tn_version", "tn_debug_gemm_tf32x3",
+           "tn_debug_network", "tn_debug_launch_counts"]
 
 _lib = None
 
@@ -90,6 +95,8 @@ def lib():
     L.tn_profile_slice.argtypes = [c.c_void_p, c.c_uint64, P(TnLaunchStat), c.c_int32, P(c.c_int32)]
     L.tn_sample.argtypes = [c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_uint64, P(c.c_uint64),
                             P(c.c_double)]
+    L.tn_sample_report.argtypes = [c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_uint64, c.c_int32, c.c_int32,
+                                   P(c.c_uint64), P(c.c_int64), P(TnReport)]
     L.tn_destroy.argtypes = [c.c_void_p]
     L.tn_destroy.restype = None
     L.tn_last_error.argtypes = [c.c_void_p]
@@ -100,7 +107,7 @@ def lib():
     L.tn_debug_network.argtypes = [c.c_void_p, P(c.c_int64), P(c.c_int64), P(c.c_int64)]
     L.tn_debug_launch_counts.argtypes = [c.c_void_p, P(c.c_int64), P(c.c_int64)]
     for name in ("tn_build", "tn_plan", "tn_plan_dump", "tn_bind_device", "tn_contract", "tn_profile_slice",
-                 "tn_sample", "tn_debug_gemm_tf32x3", "tn_debug_network", "tn_debug_launch_counts"):
+                 "tn_sample", "tn_sample_report", "tn_debug_gemm_tf32x3", "tn_debug_network", "tn_debug_launch_counts"):
         getattr(L, name).restype = c.c_int
     _lib = L
     return L
@@ -278,6 +285,24 @@ class SparseState:
                                     int(n_slices_summed), int(seed),
                                     out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), est))
         return out, {"fraction": est[0], "F_norm": est[1], "xeb": est[2]}
+
+    def sample_report(self, amps: np.ndarray, n_slices_summed: int, seed: int, sampler: str = "categorical",
+                      steps: int = 200, ideal: Optional[np.ndarray] = None):
+        """tn_sample_report: (samples, indices j into the request, estimator dict); sampler "categorical"
+        (frugal within a group) or "metropolis" (uniform-proposal chain of `steps` steps)."""
+        a = np.ascontiguousarray(amps, dtype=np.complex64)
+        idl = None if ideal is None else np.ascontiguousarray(ideal, dtype=np.complex64)
+        L = self.M // self.l
+        out = np.zeros(L, dtype=np.uint64)
+        idx = np.zeros(L, dtype=np.int64)
+        rep = TnReport()
+        self._check(lib().tn_sample_report(self._ctx, ctypes.c_void_p(a.ctypes.data),
+                                           None if idl is None else ctypes.c_void_p(idl.ctypes.data),
+                                           int(n_slices_summed), int(seed),
+                                           {"categorical": 0, "metropolis": 1}[sampler], int(steps),
+                                           out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                           idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ctypes.byref(rep)))
+        return out, idx, {name: getattr(rep, name) for name, _ in TnReport._fields_}
 
 
 def debug_gemm(A, B, embed_a: int = 0):

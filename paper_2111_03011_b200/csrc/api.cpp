@@ -40,6 +40,7 @@ inline uint64_t mix64(uint64_t z) {
 inline uint64_t rng_key(uint64_t seed, uint64_t tag) { return mix64(seed ^ (tag * 0xD1B54A32D192ED03ull)); }
 inline uint64_t rng_word(uint64_t key, uint64_t i) { return mix64(key + (i + 1) * 0x9E3779B97F4A7C15ull); }
 constexpr uint64_t TAG_SAMPLER = 4;
+constexpr uint64_t TAG_METROPOLIS = 5;
 
 }  // namespace
 
@@ -245,56 +246,116 @@ tn_status tn_profile_slice(tn_ctx* ctx, uint64_t slice_id, tn_launch_stat* stats
     return TN_OK;
 }
 
-tn_status tn_sample(const tn_ctx* cctx, const float* amps, const float* ideal_amps, int64_t n_slices_summed,
-                    uint64_t seed, uint64_t* samples_out, double est[3]) {
+tn_status tn_sample_report(const tn_ctx* cctx, const float* amps, const float* ideal_amps, int64_t n_slices_summed,
+                           uint64_t seed, int32_t sampler, int32_t steps, uint64_t* samples_out, int64_t* index_out,
+                           tn_report* rep) {
     tn_ctx* ctx = const_cast<tn_ctx*>(cctx);
-    if (!ctx || !amps || !samples_out || !est) return TN_EINVAL;
+    if (!ctx || !amps || !samples_out || !rep) return TN_EINVAL;
     const tnb::Request& r = ctx->req;
     if (r.M < 1) return fail(ctx, TN_EINVAL, "tn_sample before tn_build");
     const int s = ctx->planned ? (int)ctx->plan.sliced.size() : 0;
     if (n_slices_summed < 1 || (s < 63 && n_slices_summed > (1ll << s)))
         return fail(ctx, TN_EINVAL, "n_slices_summed must be in [1, 2^s]");
+    if (sampler != 0 && sampler != 1) return fail(ctx, TN_EINVAL, "sampler must be 0 (categorical) or 1 (Metropolis)");
+    if (sampler == 1 && steps < 1) return fail(ctx, TN_EINVAL, "Metropolis needs steps >= 1");
+    auto w_of = [&](const float* a, int64_t mu) {
+        const double re = (double)a[2 * mu], im = (double)a[2 * mu + 1];
+        return re * re + im * im;
+    };
+    auto u53 = [](uint64_t w) { return (double)(w >> 11) * (1.0 / 9007199254740992.0); };
     const uint64_t key = rng_key(seed, TAG_SAMPLER);
-    double norm2 = 0.0, xeb_sum = 0.0;
+    const uint64_t mkey = rng_key(seed, TAG_METROPOLIS);
+    const uint64_t stride = 2 * (uint64_t)std::max(steps, 0) + 1;
+    std::vector<int64_t> pick_j(r.L);
+    double norm2 = 0.0;
     for (int64_t g = 0; g < r.L; g++) {
         const float* a = amps + 2 * g * r.l;
         // weights |a|^2 = re*re + im*im in fp64, cumulated in ascending mu
         double tot = 0.0;
-        for (int64_t mu = 0; mu < r.l; mu++) {
-            const double re = (double)a[2 * mu], im = (double)a[2 * mu + 1];
-            const double w = re * re + im * im;
-            tot += w;
-        }
+        for (int64_t mu = 0; mu < r.l; mu++) tot += w_of(a, mu);
         if (!(tot > 0.0)) {
             std::ostringstream o;
             o << "all-zero group " << g;
             return fail(ctx, TN_ENUMERIC, o.str());
         }
         norm2 += tot;
-        const double u = (double)(rng_word(key, (uint64_t)g) >> 11) * (1.0 / 9007199254740992.0);
-        const double thr = u * tot;
-        double cum = 0.0;
         int64_t pick = r.l - 1;
-        for (int64_t mu = 0; mu < r.l; mu++) {
-            const double re = (double)a[2 * mu], im = (double)a[2 * mu + 1];
-            const double w = re * re + im * im;
-            cum += w;
-            if (cum > thr) {
-                pick = mu;
-                break;
+        if (sampler == 0) {
+            const double thr = u53(rng_word(key, (uint64_t)g)) * tot;
+            double cum = 0.0;
+            for (int64_t mu = 0; mu < r.l; mu++) {
+                cum += w_of(a, mu);
+                if (cum > thr) {
+                    pick = mu;
+                    break;
+                }
             }
+        } else {
+            const uint64_t c0 = (uint64_t)g * stride;
+            auto idx = [&](uint64_t c) { return std::min<int64_t>(r.l - 1, (int64_t)(u53(rng_word(mkey, c)) * (double)r.l)); };
+            int64_t x = idx(c0);
+            double wx = w_of(a, x);
+            for (int t = 1; t <= steps; t++) {
+                const int64_t y = idx(c0 + 2 * (uint64_t)t - 1);
+                const double wy = w_of(a, y);
+                if (u53(rng_word(mkey, c0 + 2 * (uint64_t)t)) * wx < wy) {
+                    x = y;
+                    wx = wy;
+                }
+            }
+            pick = x;
         }
-        const int64_t j = g * r.l + pick;
-        samples_out[g] = r.bits[j];
-        if (ideal_amps) {
-            const double re = ideal_amps[2 * j], im = ideal_amps[2 * j + 1];
-            xeb_sum += re * re + im * im;
-        }
+        pick_j[g] = g * r.l + pick;
     }
     const double N = std::ldexp(1.0, r.n);
-    est[0] = (double)n_slices_summed / std::ldexp(1.0, s);
-    est[1] = N / (double)r.M * norm2;
-    est[2] = ideal_amps ? N / (double)r.L * xeb_sum - 1.0 : std::nan("");
+    const double nan = std::nan("");
+    rep->f = (double)n_slices_summed / std::ldexp(1.0, s);
+    rep->F_norm = N / (double)r.M * norm2;
+    // phat_j = |a_j|^2 / F_norm (a distribution over all 2^n bitstrings, estimated from the M requested)
+    const double Z = rep->F_norm;
+    double hs = 0.0, xs = 0.0, ls = 0.0;
+    for (int64_t g = 0; g < r.L; g++) {
+        const int64_t j = pick_j[g];
+        samples_out[g] = r.bits[j];
+        if (index_out) index_out[g] = j;
+        hs -= std::log(w_of(amps, j) / Z);
+        if (ideal_amps) {
+            const double P = w_of(ideal_amps, j);
+            xs += P;
+            ls += std::log(N * P);
+        }
+    }
+    constexpr double kEulerGamma = 0.57721566490153286061;
+    rep->entropy_samples = hs / (double)r.L;
+    rep->xeb = ideal_amps ? N / (double)r.L * xs - 1.0 : nan;
+    rep->log_xeb = ideal_amps ? ls / (double)r.L + kEulerGamma : nan;
+    double hst = 0.0;
+    std::vector<double> x(r.M);
+    for (int64_t j = 0; j < r.M; j++) {
+        const double p = w_of(amps, j) / Z;
+        if (p > 0) hst -= p * std::log(p);
+        x[j] = N * p;
+    }
+    rep->entropy_state = N / (double)r.M * hst;
+    std::sort(x.begin(), x.end());
+    double ks = 0.0;
+    for (int64_t j = 0; j < r.M; j++) {
+        const double F = -std::expm1(-x[j]);  // 1 - e^-x
+        ks = std::max(ks, std::max((double)(j + 1) / (double)r.M - F, F - (double)j / (double)r.M));
+    }
+    rep->pt_ks = ks;
+    return TN_OK;
+}
+
+tn_status tn_sample(const tn_ctx* ctx, const float* amps, const float* ideal_amps, int64_t n_slices_summed,
+                    uint64_t seed, uint64_t* samples_out, double est[3]) {
+    if (!est) return TN_EINVAL;
+    tn_report rep;
+    const tn_status st = tn_sample_report(ctx, amps, ideal_amps, n_slices_summed, seed, 0, 0, samples_out, nullptr, &rep);
+    if (st != TN_OK) return st;
+    est[0] = rep.f;
+    est[1] = rep.F_norm;
+    est[2] = rep.xeb;
     return TN_OK;
 }
 

@@ -225,3 +225,41 @@ def test_host_sampler_matches_oracle(T):
     with pytest.raises(T.TnError) as e:
         ss.sample(zero, 1, 0)
     assert e.value.status == T.TN_ENUMERIC
+
+
+def test_sample_report_matches_oracle(T):
+    """tn_sample_report (NEXT-4 validation suite) against the oracle on the same amplitudes: the
+    categorical and the Metropolis samples are bit-exact (same counter-based generator, same fp64
+    decisions); every estimator equals the oracle's definition."""
+    from oracle import metrics
+    c = configs.get(2)
+    circ = c.circuit()
+    n = circ["n"]
+    bits = c.bitstrings(n)
+    ss = T.SparseState(circ, bits, c.open_mask(n))
+    ss.plan(1 << c.log2_tmax, n_sliced=c.n_sliced)
+    r = np.random.default_rng(21)
+    M = len(bits)
+    amps = ((r.normal(size=M) + 1j * r.normal(size=M)) * 2 ** -10).astype(np.complex64)
+    ideal = ((r.normal(size=M) + 1j * r.normal(size=M)) * 2 ** -10).astype(np.complex64)
+    l = 64
+    ph = metrics.phat(amps, n)
+    P = ideal.real.astype(float) ** 2 + ideal.imag.astype(float) ** 2
+    for sampler, steps in (("categorical", 0), ("metropolis", 1), ("metropolis", 200)):
+        samples, idx, rep = ss.sample_report(amps, 16, 3001, sampler=sampler, steps=steps, ideal=ideal)
+        want = (metrics.sample_groups(amps, l, 3001) if sampler == "categorical"
+                else metrics.metropolis_groups(amps, l, 3001, steps))
+        np.testing.assert_array_equal(idx, want)
+        np.testing.assert_array_equal(samples, bits[want])
+        assert rep["f"] == 1.0
+        assert abs(rep["F_norm"] / metrics.f_norm(amps, n) - 1) < 1e-12
+        assert abs(rep["xeb"] - metrics.linear_xeb(P[want], n)) < 1e-9 * (1 + abs(rep["xeb"]))
+        assert abs(rep["log_xeb"] - metrics.log_xeb(P[want], n)) < 1e-9
+        assert abs(rep["entropy_samples"] / metrics.entropy_samples(ph[want]) - 1) < 1e-12
+        assert abs(rep["entropy_state"] / metrics.entropy_state(ph, n) - 1) < 1e-12
+        assert abs(rep["pt_ks"] - metrics.porter_thomas_ks((2.0 ** n) * ph)) < 1e-12
+    _, _, rep = ss.sample_report(amps, 16, 1, sampler="metropolis", steps=10)
+    assert np.isnan(rep["xeb"]) and np.isnan(rep["log_xeb"])
+    with pytest.raises(T.TnError) as e:
+        ss.sample_report(amps, 16, 1, sampler="metropolis", steps=0)
+    assert e.value.status == T.TN_EINVAL

@@ -368,3 +368,77 @@ def test_config_structure():
     assert [cc.count_fsim(configs.get(k).circuit()) for k in (1, 2, 3, 4, 5)] == [17, 62, 147, 301, 430]
     b = configs.get(2).bitstrings(20)
     assert len(b) == 4096 and len(np.unique(b)) == 4096
+
+
+# ------------------------------------------------------------------------------ validation suite (NEXT-4)
+
+def test_metropolis_degenerate_group():
+    """l=2 with p=(1,0) -> always index 0 (a chain that starts on the zero-weight index
+    moves as soon as index 0 is proposed and never leaves it)."""
+    from oracle import metrics
+    amps = np.tile(np.array([1.0, 0.0], dtype=np.complex64), 4096)
+    idx = metrics.metropolis_groups(amps, 2, seed=11, steps=64)
+    assert np.all(idx % 2 == 0)
+
+
+def test_metropolis_stationary_distribution():
+    """the chain's stationary distribution is p (detailed balance of min(1, p'/p) with a
+    symmetric proposal): l=4, p=(.4,.3,.2,.1), total variation of the empirical sample distribution."""
+    from oracle import metrics
+    p = np.array([0.4, 0.3, 0.2, 0.1])
+    G = 20000
+    amps = np.tile(np.sqrt(p).astype(np.complex64), G)
+    idx = metrics.metropolis_groups(amps, 4, seed=5, steps=50)
+    emp = np.bincount(idx % 4, minlength=4) / G
+    assert 0.5 * np.abs(emp - p).sum() < 0.02
+    # and it mixes: with 1 step the start (uniform) is still visible
+    emp1 = np.bincount(metrics.metropolis_groups(amps, 4, seed=5, steps=1) % 4, minlength=4) / G
+    assert 0.5 * np.abs(emp1 - p).sum() > 0.05
+
+
+def test_metropolis_agrees_with_categorical_on_pt_groups():
+    """Metropolis and the categorical draw agree in distribution on random (Porter-Thomas)
+    groups: the linear XEB of both sample sets under the source state agree (both ~ 1)."""
+    from oracle import metrics
+    r = np.random.default_rng(3)
+    l, G, n = 64, 4000, 12
+    amps = ((r.normal(size=l * G) + 1j * r.normal(size=l * G)) / np.sqrt(2 * (1 << n))).astype(np.complex64)
+    ph = metrics.phat(amps, n)
+    x_cat = metrics.linear_xeb(ph[metrics.sample_groups(amps, l, 7)], n)
+    x_met = metrics.linear_xeb(ph[metrics.metropolis_groups(amps, l, 7, 200)], n)
+    assert abs(x_cat - 1.0) < 0.1 and abs(x_met - 1.0) < 0.1 and abs(x_cat - x_met) < 0.1
+
+
+def test_log_xeb_closed_forms():
+    """log XEB = <ln(N P)> + gamma: perfect Porter-Thomas sampling (N P ~ Gamma(2,1), size-biased Exp)
+    gives psi(2) + gamma = 1; uniform sampling (N P ~ Exp(1)) gives psi(1) + gamma = 0."""
+    from oracle import metrics
+    r = np.random.default_rng(9)
+    n, L = 20, 200000
+    N = 2.0 ** n
+    assert abs(metrics.log_xeb(r.gamma(2.0, 1.0, L) / N, n) - 1.0) < 0.01
+    assert abs(metrics.log_xeb(r.exponential(1.0, L) / N, n)) < 0.01
+
+
+def test_entropy_closed_forms():
+    """Uniform distribution over the 2^n strings, observed on a subset of M = 256 of them (the sparse
+    state): H_state = H_samples = n ln 2 (this needs the 2^n/M factor); a delta: 0."""
+    from oracle import metrics
+    n = 10
+    amps = np.full(256, 2.0 ** (-n / 2), dtype=np.complex64)
+    ph = metrics.phat(amps, n)
+    assert abs(metrics.entropy_state(ph, n) - n * math.log(2)) < 1e-9
+    assert abs(metrics.entropy_samples(ph[:100]) - n * math.log(2)) < 1e-9
+    d = np.zeros(1 << n, dtype=np.complex64)
+    d[5] = 1
+    pd = metrics.phat(d, n)
+    assert abs(metrics.entropy_state(pd, n)) < 1e-12 and abs(metrics.entropy_samples(pd[[5]])) < 1e-12
+
+
+def test_porter_thomas_ks_closed_forms():
+    """KS distance to Exp(1): exact Exp(1) draws -> small (< 1.63/sqrt(m) at 1 %); a constant x = 1 ->
+    max(F(1), 1 - F(1)) = F(1) = 1 - e^-1 = 0.632."""
+    from oracle import metrics
+    r = np.random.default_rng(2)
+    assert metrics.porter_thomas_ks(r.exponential(1.0, 100000)) < 1.63 / math.sqrt(100000)
+    assert abs(metrics.porter_thomas_ks(np.ones(1000)) - (1 - math.exp(-1))) < 1e-12

@@ -24,6 +24,7 @@ TAG_GATES = 1
 TAG_FSIM = 2
 TAG_BITS = 3
 TAG_SAMPLER = 4
+TAG_METROPOLIS = 5
 
 
 def mix64(z: int) -> int:
