@@ -87,6 +87,17 @@ typedef struct {
 tn_status tn_build(const tn_circuit* circuit, const uint64_t* bitstrings, int64_t M,
                    uint64_t open_mask, tn_ctx** out);
 
+/* tn_build_drilled -- tn_build on the network with K/2 holes drilled (Fig. 1 "each hole is
+ * created by breaking two edges"; case (i) P:L106-L109).  holes[h] indexes circuit->gates and must be
+ * an fSim gate; both of its input edges are broken, E = (1,0)x(1,0) inserted on each qubit right before
+ * the gate (after its pending single-qubit gates).  Because fSim|00> = |00>, the gate then drops out of the
+ * network exactly: each of its wires carries |0><0| U and the two qubits decouple at that gate.  Wire ids
+ * are unchanged (the drilled gate still counts on both wires).  The estimated fidelity of the result is
+ * 2^-2 per hole times the slice fraction.  EINVAL on a hole that is out of range, not an fSim, or
+ * repeated; otherwise as tn_build. */
+tn_status tn_build_drilled(const tn_circuit* circuit, const uint64_t* bitstrings, int64_t M, uint64_t open_mask,
+                           const int32_t* holes, int32_t n_holes, tn_ctx** out);
+
 typedef struct {
     int32_t n_sliced;            /* -1: the minimal s meeting max_tensor_size; else exactly s  */
     int32_t n_forced;            /* sliced wires forced first (in this order)                 */

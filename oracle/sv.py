@@ -139,12 +139,30 @@ def slice_insertions(wires: Sequence[Tuple[int, int]], sigma: int) -> List[Tuple
     return [(q, k, v) for (q, k), v in zip(wires, slice_values(sigma, s))]
 
 
+def hole_insertions(circuit: dict, holes: Sequence[int]) -> List[Tuple[int, int, int]]:
+    """A drilled hole (Fig. 1) breaks both input edges of one fSim gate: E = (1,0)x(1,0),
+    i.e. Pi_0 on each of its two qubits right before the gate (after the gates already on the wire).
+    holes index the circuit's gates flattened moment by moment."""
+    flat = [g for m in circuit["moments"] for g in m]
+    ins = []
+    for h in holes:
+        g = flat[h]
+        if g["type"] != "fsim":
+            raise ValueError("a hole must be an fSim gate")
+        for q in g["targets"]:
+            before = sum(1 for x in flat[:h] if (x["target"] == q if x["type"] == "single" else q in x["targets"]))
+            ins.append((q, before, 0))
+    return ins
+
+
 def sliced_amplitudes(circuit: dict, bitstrings: np.ndarray, wires: Sequence[Tuple[int, int]],
-                      subset: Iterable[int], threads: int = 0) -> np.ndarray:
-    """amp_S(x_j) = sum over sigma in S (ascending) of <x_j|U_sigma|0> (one state-vector run per sigma)."""
+                      subset: Iterable[int], threads: int = 0,
+                      extra: Sequence[Tuple[int, int, int]] = ()) -> np.ndarray:
+    """amp_S(x_j) = sum over sigma in S (ascending) of <x_j|U_sigma|0> (one state-vector run per sigma);
+    `extra` insertions (e.g. drilled holes) apply to every run."""
     acc = np.zeros(len(bitstrings), dtype=complex)
     for sigma in sorted(set(int(x) for x in subset)):
-        a, _ = amplitudes(circuit, bitstrings, slice_insertions(wires, sigma), threads)
+        a, _ = amplitudes(circuit, bitstrings, list(extra) + slice_insertions(wires, sigma), threads)
         acc += a
     return acc
 

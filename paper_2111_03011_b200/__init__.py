@@ -70,7 +70,7 @@ class TnReport(ctypes.Structure):
                 ("f", "F_norm", "xeb", "log_xeb", "entropy_samples", "entropy_state", "pt_ks")]
 
 
-EXPORTS = ["tn_build", "tn_plan", "tn_plan_dump", "tn_bind_device", "tn_contract", "tn_profile_slice",
+EXPORTS = ["tn_build", "tn_build_drilled", "tn_plan", "tn_plan_dump", "tn_bind_device", "tn_contract", "tn_profile_slice",
            "tn_sample", "tn_sample_report", "tn_destroy", "tn_last_error", "tn_version", "tn_debug_gemm_tf32x3",
            "tn_debug_network", "tn_debug_launch_counts"]
 
@@ -88,6 +88,8 @@ def lib():
     L = ctypes.CDLL(LIB_PATH)
     P, c = ctypes.POINTER, ctypes
     L.tn_build.argtypes = [P(TnCircuit), P(c.c_uint64), c.c_int64, c.c_uint64, P(c.c_void_p)]
+    L.tn_build_drilled.argtypes = [P(TnCircuit), P(c.c_uint64), c.c_int64, c.c_uint64, P(c.c_int32), c.c_int32,
+                                   P(c.c_void_p)]
     L.tn_plan.argtypes = [c.c_void_p, P(TnSlicing), c.c_int64, P(TnPlanInfo)]
     L.tn_plan_dump.argtypes = [c.c_void_p, c.c_char_p]
     L.tn_bind_device.argtypes = [c.c_void_p, c.c_int, c.c_void_p, c.c_size_t, c.c_void_p]
@@ -106,7 +108,7 @@ def lib():
                                        c.c_int32, c.c_void_p]
     L.tn_debug_network.argtypes = [c.c_void_p, P(c.c_int64), P(c.c_int64), P(c.c_int64)]
     L.tn_debug_launch_counts.argtypes = [c.c_void_p, P(c.c_int64), P(c.c_int64)]
-    for name in ("tn_build", "tn_plan", "tn_plan_dump", "tn_bind_device", "tn_contract", "tn_profile_slice",
+    for name in ("tn_build", "tn_build_drilled", "tn_plan", "tn_plan_dump", "tn_bind_device", "tn_contract", "tn_profile_slice",
                  "tn_sample", "tn_sample_report", "tn_debug_gemm_tf32x3", "tn_debug_network", "tn_debug_launch_counts"):
         getattr(L, name).restype = c.c_int
     _lib = L
@@ -149,7 +151,9 @@ def circuit_struct(circuit: dict):
 class SparseState:
     """One sparse-state contraction context (tn_ctx).  Single-threaded; one per GPU / rank."""
 
-    def __init__(self, circuit: dict, bitstrings: np.ndarray, open_mask: int = 0):
+    def __init__(self, circuit: dict, bitstrings: np.ndarray, open_mask: int = 0, holes: Sequence[int] = ()):
+        """tn_build, or tn_build_drilled when `holes` lists fSim gates (indices into the flattened gate
+        list, moment by moment) to drill out."""
         L = lib()
         self._circ = circuit_struct(circuit)
         self.bitstrings = np.ascontiguousarray(bitstrings, dtype=np.uint64)
@@ -157,9 +161,12 @@ class SparseState:
         self.n = circuit["n"]
         self.open_mask = int(open_mask)
         self.l = 1 << bin(self.open_mask).count("1")
+        self.holes = [int(h) for h in holes]
         self._ctx = ctypes.c_void_p()
-        rc = L.tn_build(ctypes.byref(self._circ), self.bitstrings.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
-                        self.M, self.open_mask, ctypes.byref(self._ctx))
+        harr = (ctypes.c_int32 * max(1, len(self.holes)))(*self.holes)
+        rc = L.tn_build_drilled(ctypes.byref(self._circ),
+                                self.bitstrings.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), self.M,
+                                self.open_mask, harr, len(self.holes), ctypes.byref(self._ctx))
         if rc != TN_OK:
             msg = self.last_error()
             self.close()

@@ -58,6 +58,11 @@ void tn_destroy(tn_ctx* ctx) {
 
 tn_status tn_build(const tn_circuit* circuit, const uint64_t* bitstrings, int64_t M, uint64_t open_mask,
                    tn_ctx** out) {
+    return tn_build_drilled(circuit, bitstrings, M, open_mask, nullptr, 0, out);
+}
+
+tn_status tn_build_drilled(const tn_circuit* circuit, const uint64_t* bitstrings, int64_t M, uint64_t open_mask,
+                           const int32_t* holes, int32_t n_holes, tn_ctx** out) {
     if (!out) return TN_EINVAL;
     *out = nullptr;
     tn_ctx* c = new tn_ctx();
@@ -107,7 +112,8 @@ tn_status tn_build(const tn_circuit* circuit, const uint64_t* bitstrings, int64_
     std::sort(r.fixed.begin(), r.fixed.end());
     r.fixed.erase(std::unique(r.fixed.begin(), r.fixed.end()), r.fixed.end());
 
-    std::string e = tnb::build_network(circuit, c->net);
+    if (n_holes < 0 || (n_holes > 0 && !holes)) return fail(c, TN_EINVAL, "bad hole list");
+    std::string e = tnb::build_network(circuit, c->net, std::vector<int32_t>(holes, holes + n_holes));
     if (!e.empty()) return fail(c, TN_EINVAL, e);
     for (auto& E : c->net.edges)
         if (E.output && ((open_mask >> (n - 1 - E.q)) & 1)) E.open = true;

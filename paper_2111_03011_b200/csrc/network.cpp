@@ -107,8 +107,15 @@ HTensor contract_host(const HTensor& A, const HTensor& B) {
     return C;
 }
 
-std::string build_network(const tn_circuit* c, Network& net) {
+std::string build_network(const tn_circuit* c, Network& net, const std::vector<int32_t>& holes) {
     const int n = c->n_qubits;
+    std::set<int> hole_set;
+    for (int32_t h : holes) {
+        const int ng = c->n_moments > 0 ? c->moment_offsets[c->n_moments] : 0;
+        if (h < 0 || h >= ng) return "hole index out of range";
+        if (c->gates[h].kind != 1) return "a hole must be an fSim gate";
+        if (!hole_set.insert(h).second) return "hole listed twice";
+    }
     if (n < 1 || n > 63) return "n_qubits must be in [1, 63]";
     if (c->n_moments < 0 || (c->n_moments > 0 && (!c->moment_offsets || !c->gates)))
         return "bad moment arrays";
@@ -154,6 +161,20 @@ std::string build_network(const tn_circuit* c, Network& net) {
             const int a = G.q0, b = G.q1;
             gcount[a]++;
             gcount[b]++;
+            if (hole_set.count(g)) {
+                // drilled hole (case (i) P:L106-L109): both input edges broken by
+                // E = (1,0)x(1,0) right before the gate; fSim|00> = |00>, so the gate drops out exactly and
+                // each wire carries |0><0| U (its pending single-qubit gates, then the break)
+                for (int q : {a, b}) {
+                    Mat2 pin;
+                    pin.m[0][0] = 1.0;
+                    pin.m[0][1] = 0.0;
+                    pin.m[1][0] = 0.0;
+                    pin.m[1][1] = 0.0;
+                    P[q] = mul(pin, P[q]);
+                }
+                continue;
+            }
             cd F[4][4];
             fsim_matrix(G.theta, G.phi, F);
             HTensor T;

@@ -58,7 +58,8 @@ struct Request {
 // absorbed into the next tensor on the wire, the final layer into the previous one) and
 // simplify it (order-1 and order-2 tensors contracted into neighbours).
 // Returns an empty string on success, else an error message.
-std::string build_network(const tn_circuit* c, Network& net);
+// holes: indices into c->gates of fSim gates drilled out (both input edges broken)
+std::string build_network(const tn_circuit* c, Network& net, const std::vector<int32_t>& holes = {});
 void simplify(Network& net);
 std::vector<Leaf> make_leaves(const Network& net, const Request& req);
 

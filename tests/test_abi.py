@@ -263,3 +263,22 @@ def test_sample_report_matches_oracle(T):
     with pytest.raises(T.TnError) as e:
         ss.sample_report(amps, 16, 1, sampler="metropolis", steps=0)
     assert e.value.status == T.TN_EINVAL
+
+
+def test_drilled_holes_shrink_the_network(T):
+    """tn_build_drilled (NEXT-3): drilling fSim gates removes them from the network (fewer
+    tensors and sliceable edges); bad hole lists are rejected."""
+    c = configs.get(3)
+    circ = c.circuit()
+    n = circ["n"]
+    flat = [g for m in circ["moments"] for g in m]
+    fs = [i for i, g in enumerate(flat) if g["type"] == "fsim"]
+    holes = [fs[len(fs) // 2 - 3], fs[len(fs) // 2 + 3]]
+    base = T.SparseState(circ, c.bitstrings(n), c.open_mask(n))
+    drilled = T.SparseState(circ, c.bitstrings(n), c.open_mask(n), holes=holes)
+    a, b = base.network_size(), drilled.network_size()
+    assert b["tensors"] < a["tensors"] and b["internal_edges"] < a["internal_edges"]
+    for bad in ([0], [holes[0], holes[0]], [len(flat)]):  # gate 0 is a single-qubit gate
+        with pytest.raises(T.TnError) as e:
+            T.SparseState(circ, c.bitstrings(n), c.open_mask(n), holes=bad)
+        assert e.value.status == T.TN_EINVAL

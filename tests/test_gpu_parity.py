@@ -315,3 +315,28 @@ def test_edge_bad_slice_subsets(T):
             ss.contract(bad)
         assert e.value.status == T.TN_EINVAL
     ss.contract([15])  # still usable after rejected calls
+
+
+# ------------------------------------------------------------------------------ drilled holes (NEXT-3)
+
+def test_drilled_holes_match_oracle(T, oracle_built):
+    """tn_build_drilled: the network with holes drilled at two mid-circuit fSim gates equals
+    the oracle's state vector with Pi_0 on both input edges of each drilled gate -- all slices summed
+    and a prefix (the breaks compose with slicing)."""
+    from oracle import sv
+    c = configs.get(2)
+    circ = c.circuit()
+    n = circ["n"]
+    bits = c.bitstrings(n)
+    flat = [g for m in circ["moments"] for g in m]
+    fs = [i for i, g in enumerate(flat) if g["type"] == "fsim"]
+    holes = [fs[len(fs) // 2], fs[len(fs) // 2 + 5]]
+    ss = T.SparseState(circ, bits, c.open_mask(n), holes=holes)
+    info = ss.plan(1 << c.log2_tmax, n_sliced=4, seed=1)
+    ss.bind(0)
+    s = info["s"]
+    ins = sv.hole_insertions(circ, holes)
+    want, _ = sv.amplitudes(circ, bits, ins)
+    assert_amps_close(ss.contract(range(1 << s)).cpu().numpy(), want)
+    want2 = sv.sliced_amplitudes(circ, bits, info["sliced_wires"], range(1 << (s - 2)), extra=ins)
+    assert_amps_close(ss.contract(range(1 << (s - 2))).cpu().numpy(), want2)

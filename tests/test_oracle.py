@@ -442,3 +442,53 @@ def test_porter_thomas_ks_closed_forms():
     r = np.random.default_rng(2)
     assert metrics.porter_thomas_ks(r.exponential(1.0, 100000)) < 1.63 / math.sqrt(100000)
     assert abs(metrics.porter_thomas_ks(np.ones(1000)) - (1 - math.exp(-1))) < 1e-12
+
+
+# ------------------------------------------------------------------------------ drilled holes (NEXT-3)
+
+def _fsim_indices(circuit):
+    flat = [g for m in circuit["moments"] for g in m]
+    return [i for i, g in enumerate(flat) if g["type"] == "fsim"]
+
+
+def _without_gate(circuit, h):
+    """The same circuit with flattened gate h deleted."""
+    out, i = [], 0
+    for m in circuit["moments"]:
+        mm = []
+        for g in m:
+            if i != h:
+                mm.append(g)
+            i += 1
+        out.append(mm)
+    c = dict(circuit)
+    c["moments"] = out
+    return c
+
+
+def test_hole_removes_the_gate_exactly(oracle_built):
+    """PAPER.md L106-L109, case (i): with both input edges of an fSim broken (Pi_0 (x) Pi_0 right before
+    it), the gate evaluates to |00><00| -- it can be replaced by (1,0) vectors: the state equals that of
+    the circuit with the gate deleted and the same two projectors."""
+    from oracle import sv
+    c = small_circuit(3, 3, 8, 71)
+    fs = _fsim_indices(c)
+    for h in (fs[len(fs) // 3], fs[2 * len(fs) // 3]):
+        ins = sv.hole_insertions(c, [h])
+        a = sv.statevector(c, ins)
+        b = sv.statevector(_without_gate(c, h), ins)
+        assert np.max(np.abs(a - b)) < 1e-12
+        assert np.linalg.norm(a) > 0.05  # a nontrivial state survives
+
+
+def test_hole_fidelity_quarter(oracle_built):
+    """PAPER.md L73 / Fig. 1: each broken edge halves the fidelity, so one hole (two edges) gives
+    F ~ 1/4; ensemble mean over random 12-qubit circuits with a hole mid-circuit."""
+    from oracle import metrics, sv
+    Fs = []
+    for seed in range(10):
+        c = small_circuit(3, 4, 12, 300 + seed)
+        fs = _fsim_indices(c)
+        h = fs[len(fs) // 2]
+        Fs.append(metrics.f_exact(sv.statevector(c), sv.statevector(c, sv.hole_insertions(c, [h]))))
+    assert 0.15 < np.mean(Fs) < 0.4, Fs
