@@ -105,6 +105,12 @@ typedef struct {
     uint64_t seed;               /* planner randomisation seed                                */
     int32_t trials;              /* randomized greedy restarts (<= 0: default)                */
     double time_budget_s;        /* planner wall-clock budget (<= 0: default)                 */
+    int32_t companions;          /* 1: companion-edge rank-one truncation: for each
+                                    sliced wire that is an output of an fSim G, the input edge of G
+                                    on the other qubit is projected onto the dominant singular vector
+                                    of the pinned gate, i.e. onto |v> in G's input basis with v the
+                                    sliced wire's value (cutting that companion edge too); fidelity
+                                    factor (1 + sin^2 theta)/2 each                      */
 } tn_slicing;
 
 typedef struct {
@@ -120,6 +126,11 @@ typedef struct {
     double gemm_cmac_per_slice;  /* part of cmac_per_slice on the tensor-core GEMM path       */
     int64_t n_invariant_steps;   /* steps with no sliced edge below them: run once per        */
     double invariant_cmac;       /* tn_contract, before the slices (their CMACs)              */
+    int32_t n_companions;        /* companion edges cut (tn_slicing.companions)               */
+    const int32_t* companion_wires; /* 3*n ints: (q, k, b): Pi_v on wire (q, k) -- right before
+                                    the fSim, after its single-qubit gates -- with v = slice bit b
+                                    (owned by ctx)                                             */
+    double companion_fidelity;   /* prod (1 + sin^2 theta_i)/2 over the companions   */
 } tn_plan_info;
 
 /* tn_plan -- P:L91 (complexity-greedy contraction order), P:L246 (slicing: fix index values so

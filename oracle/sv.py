@@ -155,14 +155,41 @@ def hole_insertions(circuit: dict, holes: Sequence[int]) -> List[Tuple[int, int,
     return ins
 
 
+def companion_of(circuit: dict, wire: Tuple[int, int]) -> Optional[Tuple[int, int]]:
+    """Companion of a sliced wire (supplement "singular values of the sliced fSim
+    gate"): if wire (q, k) is the output on q of an fSim gate G (G = the k-th gate on q) on qubits (q, b),
+    the companion edge is G's other input; the rank-one truncation keeps the dominant singular vector e_v,
+    i.e. Pi_v on qubit b right before G: wire (b, number of gates on b before G).  None otherwise."""
+    q, k = wire
+    flat = [g for m in circuit["moments"] for g in m]
+    seen = 0
+    for h, g in enumerate(flat):
+        on_q = g["target"] == q if g["type"] == "single" else q in g["targets"]
+        if not on_q:
+            continue
+        seen += 1
+        if seen == k:
+            if g["type"] != "fsim":
+                return None
+            b = g["targets"][1] if g["targets"][0] == q else g["targets"][0]
+            before = sum(1 for x in flat[:h] if (x["target"] == b if x["type"] == "single" else b in x["targets"]))
+            return (b, before)
+    return None
+
+
 def sliced_amplitudes(circuit: dict, bitstrings: np.ndarray, wires: Sequence[Tuple[int, int]],
                       subset: Iterable[int], threads: int = 0,
-                      extra: Sequence[Tuple[int, int, int]] = ()) -> np.ndarray:
+                      extra: Sequence[Tuple[int, int, int]] = (),
+                      companions: Sequence[Tuple[int, int, int]] = ()) -> np.ndarray:
     """amp_S(x_j) = sum over sigma in S (ascending) of <x_j|U_sigma|0> (one state-vector run per sigma);
-    `extra` insertions (e.g. drilled holes) apply to every run."""
+    `extra` insertions (e.g. drilled holes) apply to every run; `companions` (q, k, i) put Pi_v on wire
+    (q, k) with v the value of sliced wire i."""
     acc = np.zeros(len(bitstrings), dtype=complex)
     for sigma in sorted(set(int(x) for x in subset)):
-        a, _ = amplitudes(circuit, bitstrings, list(extra) + slice_insertions(wires, sigma), threads)
+        ins = slice_insertions(wires, sigma)
+        # companions: (q, k, i) -> Pi_v on (q, k) with v the value of sliced wire i in this slice
+        ins += [(cq, ck, ins[i][2]) for (cq, ck, i) in companions]
+        a, _ = amplitudes(circuit, bitstrings, list(extra) + ins, threads)
         acc += a
     return acc
 

@@ -47,7 +47,7 @@ class TnCircuit(ctypes.Structure):
 class TnSlicing(ctypes.Structure):
     _fields_ = [("n_sliced", ctypes.c_int32), ("n_forced", ctypes.c_int32),
                 ("forced_wires", ctypes.POINTER(ctypes.c_int32)), ("seed", ctypes.c_uint64),
-                ("trials", ctypes.c_int32), ("time_budget_s", ctypes.c_double)]
+                ("trials", ctypes.c_int32), ("time_budget_s", ctypes.c_double), ("companions", ctypes.c_int32)]
 
 
 class TnPlanInfo(ctypes.Structure):
@@ -56,7 +56,8 @@ class TnPlanInfo(ctypes.Structure):
                 ("peak_elems", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
                 ("cmac_per_slice", ctypes.c_double), ("bytes_per_slice", ctypes.c_double),
                 ("gemm_cmac_per_slice", ctypes.c_double), ("n_invariant_steps", ctypes.c_int64),
-                ("invariant_cmac", ctypes.c_double)]
+                ("invariant_cmac", ctypes.c_double), ("n_companions", ctypes.c_int32),
+                ("companion_wires", ctypes.POINTER(ctypes.c_int32)), ("companion_fidelity", ctypes.c_double)]
 
 
 class TnLaunchStat(ctypes.Structure):
@@ -198,9 +199,9 @@ class SparseState:
 
     # -------------------------------------------------------------- tn_plan
     def plan(self, max_tensor_size: int, n_sliced: int = -1, forced_wires: Sequence = (), seed: int = 1,
-             trials: int = 0, time_budget_s: float = 0.0) -> dict:
+             trials: int = 0, time_budget_s: float = 0.0, companions: bool = False) -> dict:
         fw = (ctypes.c_int32 * max(1, 2 * len(forced_wires)))(*[v for w in forced_wires for v in w])
-        sl = TnSlicing(n_sliced, len(forced_wires), fw, seed, trials, time_budget_s)
+        sl = TnSlicing(n_sliced, len(forced_wires), fw, seed, trials, time_budget_s, 1 if companions else 0)
         info = TnPlanInfo()
         self._check(lib().tn_plan(self._ctx, ctypes.byref(sl), int(max_tensor_size), ctypes.byref(info)))
         self.info = {
@@ -211,6 +212,9 @@ class SparseState:
             "cmac_per_slice": info.cmac_per_slice, "bytes_per_slice": info.bytes_per_slice,
             "gemm_cmac_per_slice": info.gemm_cmac_per_slice,
             "n_invariant_steps": info.n_invariant_steps, "invariant_cmac": info.invariant_cmac,
+            "companions": [(info.companion_wires[3 * i], info.companion_wires[3 * i + 1],
+                            info.companion_wires[3 * i + 2]) for i in range(info.n_companions)],
+            "companion_fidelity": info.companion_fidelity,
         }
         return self.info
 

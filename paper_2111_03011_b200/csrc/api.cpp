@@ -20,6 +20,7 @@ struct tn_ctx {
     tnb::Plan plan;
     tnb::Program prog;
     std::vector<int32_t> sliced_wires;
+    std::vector<int32_t> companion_wires;
     tn_plan_info info{};
     tnb::Device* dev = nullptr;
 };
@@ -165,7 +166,15 @@ tn_status tn_plan(tn_ctx* ctx, const tn_slicing* slicing, int64_t max_tensor_siz
     tnb::Plan plan;
     std::string e = tnb::find_plan(ctx->net, ctx->leaves, ctx->req, opt, plan);
     if (!e.empty()) return fail(ctx, TN_EINFEASIBLE, e);
-    e = tnb::lower_plan(ctx->net, ctx->leaves, ctx->req, plan, ctx->prog);
+    if (slicing && slicing->companions) {
+        // the companion edges change the network (exact basis changes) and the leaves: plan on a copy
+        tnb::Network net2 = ctx->net;
+        tnb::add_companions(net2, plan);
+        std::vector<tnb::Leaf> leaves2 = tnb::make_leaves(net2, ctx->req);
+        e = tnb::lower_plan(net2, leaves2, ctx->req, plan, ctx->prog);
+    } else {
+        e = tnb::lower_plan(ctx->net, ctx->leaves, ctx->req, plan, ctx->prog);
+    }
     if (!e.empty()) return fail(ctx, TN_EINVAL, e);
     ctx->plan = plan;
     ctx->planned = true;
@@ -190,6 +199,16 @@ tn_status tn_plan(tn_ctx* ctx, const tn_slicing* slicing, int64_t max_tensor_siz
     for (const auto& st : ctx->prog.pre_steps)
         if (st.kind == tnb::K_APPLY || st.kind == tnb::K_GEMM) I.n_invariant_steps++;
     I.invariant_cmac = ctx->prog.pre_cmac;
+    ctx->companion_wires.clear();
+    I.companion_fidelity = 1.0;
+    for (size_t t = 0; t < plan.tied.size(); t++) {
+        ctx->companion_wires.push_back(plan.tied_wire[t].first);
+        ctx->companion_wires.push_back(plan.tied_wire[t].second);
+        ctx->companion_wires.push_back(plan.tied[t].second);
+        I.companion_fidelity *= plan.tied_factor[t];
+    }
+    I.n_companions = (int32_t)plan.tied.size();
+    I.companion_wires = ctx->companion_wires.data();
     if (info) *info = I;
     return TN_OK;
 }

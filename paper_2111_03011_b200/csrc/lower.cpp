@@ -95,6 +95,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     prog.s = s;
     std::map<int, int> slice_index;
     for (int i = 0; i < s; i++) slice_index[plan.sliced[i]] = i;
+    for (const auto& t : plan.tied) slice_index[t.first] = t.second;  // companion edges share the bit
     Alloc wa;  // per-slice workspace (reused between steps)
     Alloc pa;  // persistent region for slice-invariant results (read by every slice)
     std::vector<LT> slot(leaves.size());

@@ -28,10 +28,22 @@ struct HTensor {
     bool alive = true;
 };
 
+// One (undrilled) fSim gate of the circuit, for the companion-edge rank-one truncation:
+// its input / output edges per qubit (in = -1: the |0> input) and the single-qubit products absorbed
+// into its tensor on each input (T = fSim (P_a x P_b)).
+struct FsimRec {
+    int q[2] = {-1, -1};
+    int in[2] = {-1, -1}, out[2] = {-1, -1};
+    int kin[2] = {0, 0};  // gates on each qubit before this one: wire (q, kin) = right before the gate
+    cd P[2][2][2];  // P[i][row][col]
+    double theta = 0;
+};
+
 struct Network {
     int n = 0;
     std::vector<Edge> edges;
     std::vector<HTensor> tensors;
+    std::vector<FsimRec> fsims;
 };
 
 // A leaf of the contraction in row form: the fixed output legs of the tensor are absorbed as
@@ -58,6 +70,7 @@ struct Request {
 // absorbed into the next tensor on the wire, the final layer into the previous one) and
 // simplify it (order-1 and order-2 tensors contracted into neighbours).
 // Returns an empty string on success, else an error message.
+
 // holes: indices into c->gates of fSim gates drilled out (both input edges broken)
 std::string build_network(const tn_circuit* c, Network& net, const std::vector<int32_t>& holes = {});
 void simplify(Network& net);
@@ -80,9 +93,21 @@ struct PlanTensor {
 struct Plan {
     std::vector<std::pair<int, int>> order;  // (i, j): contract leaves/intermediates, result at i
     std::vector<int> sliced;                 // edge ids, MSB-first slice order
+    // companion edges: edge, slice bit of its partner sliced edge, fidelity factor
+    std::vector<std::pair<int, int>> tied;
+    std::vector<double> tied_factor;
+    std::vector<std::pair<int, int>> tied_wire;  // (q, k): the projector's wire, right before the gate
     double cmac = 0, bytes = 0, time_s = 0;  // per slice
     double peak = 0;                         // elements, per slice
 };
+
+// Companion-edge rank-one truncation (supplement "singular values of the sliced fSim gate"):
+// for every sliced edge that is an output of an fSim gate G on qubit a, the input edge of G on the other
+// qubit b is re-expressed in G's own input basis (the single-qubit product P_b absorbed into G's tensor
+// moves across the edge into the upstream tensor: exact for unitary P_b) and tied to the sliced edge's
+// slice bit, i.e. projected onto the dominant right singular vector e_v of the pinned gate.  Modifies
+// `net` (pass a copy) and fills plan.tied / plan.tied_factor ((1 + sin^2 theta)/2 each).
+void add_companions(Network& net, Plan& plan);
 
 struct PlanOptions {
     int n_sliced = -1;

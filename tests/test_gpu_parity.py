@@ -340,3 +340,27 @@ def test_drilled_holes_match_oracle(T, oracle_built):
     assert_amps_close(ss.contract(range(1 << s)).cpu().numpy(), want)
     want2 = sv.sliced_amplitudes(circ, bits, info["sliced_wires"], range(1 << (s - 2)), extra=ins)
     assert_amps_close(ss.contract(range(1 << (s - 2))).cpu().numpy(), want2)
+
+
+def test_companion_truncation_matches_oracle(T, oracle_built):
+    """tn_slicing.companions: every reported companion is the oracle's companion of its
+    sliced wire, and each slice / subset / prefix equals the oracle's state vector with Pi_v on the sliced
+    wire AND on its companion (v = the slice's value of that wire)."""
+    from oracle import sv
+    c = configs.get(2)
+    circ = c.circuit()
+    n = circ["n"]
+    bits = c.bitstrings(n)
+    ss = T.SparseState(circ, bits, c.open_mask(n))
+    info = ss.plan(1 << c.log2_tmax, n_sliced=4, seed=1, companions=True)
+    s = info["s"]
+    wires = info["sliced_wires"]
+    comps = info["companions"]
+    assert len(comps) >= 1
+    for (q, k, i) in comps:
+        assert sv.companion_of(circ, wires[i]) == (q, k)
+    ss.bind(0)
+    for subset in (range(1 << s), [3], range(1 << (s - 1))):
+        want = sv.sliced_amplitudes(circ, bits, wires, subset, companions=comps)
+        assert_amps_close(ss.contract(subset).cpu().numpy(), want)
+    assert 0.9 < info["companion_fidelity"] <= 1.0

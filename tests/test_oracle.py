@@ -492,3 +492,59 @@ def test_hole_fidelity_quarter(oracle_built):
         h = fs[len(fs) // 2]
         Fs.append(metrics.f_exact(sv.statevector(c), sv.statevector(c, sv.hole_insertions(c, [h]))))
     assert 0.15 < np.mean(Fs) < 0.4, Fs
+
+
+# ------------------------------------------------------------------------------ companion edges (NEXT-3)
+
+@pytest.mark.parametrize("theta", [math.pi / 2, math.pi / 3, 1.4])
+@pytest.mark.parametrize("v", [0, 1])
+def test_companion_truncation_is_the_input_projector(theta, v):
+    """Supplement: with one output of fSim pinned to v, the 3-way remainder reshaped
+    with the OTHER qubit's input as columns has squared singular values {1 + sin^2, cos^2}; its rank-one
+    truncation (SVD, keep the dominant pair) equals pinning that input to the same v (Pi_v), and keeps
+    (1 + sin^2 theta)/2 of the squared norm.  (Pinning an output and cutting the other input is the
+    transpose of the paper's cases: fSim is a symmetric matrix.)"""
+    from oracle import sv
+    F = sv.fsim_matrix(theta, math.pi / 6).reshape(2, 2, 2, 2)   # [o_a, o_b, i_a, i_b]
+    M = F[v].reshape(4, 2)                                       # rows (o_b, i_a), columns i_b
+    U, S, Vh = np.linalg.svd(M, full_matrices=False)
+    assert np.allclose(np.sort(S ** 2), np.sort([1 + math.sin(theta) ** 2, math.cos(theta) ** 2]))
+    rank1 = S[0] * np.outer(U[:, 0], Vh[0])
+    pin = M.copy()
+    pin[:, 1 - v] = 0                                            # Pi_v on the input i_b
+    assert np.allclose(rank1, pin)
+    assert abs(np.sum(np.abs(pin) ** 2) / 2 - (1 + math.sin(theta) ** 2) / 2) < 1e-12
+
+
+def _set_theta(circuit, wire, theta):
+    """Copy of the circuit with the fSim that ends sliced wire `wire` set to angle theta."""
+    import copy
+    c = copy.deepcopy(circuit)
+    q, k = wire
+    seen = 0
+    for m in c["moments"]:
+        for g in m:
+            if (g["target"] == q if g["type"] == "single" else q in g["targets"]):
+                seen += 1
+                if seen == k:
+                    g["theta"] = theta
+                    return c
+    raise AssertionError
+
+
+def test_companion_fidelity_factor(oracle_built):
+    """the companion truncation costs (1 + sin^2 theta)/2 of fidelity: exactly 1 at
+    theta = pi/2 (nothing truncated, cos theta = 0); ~0.875 at theta = pi/3 (ensemble)."""
+    from oracle import metrics, sv
+    Fs = {math.pi / 2: [], math.pi / 3: []}
+    for seed in range(8):
+        c0 = small_circuit(3, 4, 10, 500 + seed)
+        w = fsim_wires(c0)[len(fsim_wires(c0)) // 2]
+        for th in Fs:
+            c = _set_theta(c0, w, th)
+            comp = sv.companion_of(c, w)
+            psi = sv.statevector(c)
+            approx = sum(sv.statevector(c, [(w[0], w[1], v), (comp[0], comp[1], v)]) for v in (0, 1))
+            Fs[th].append(metrics.f_exact(psi, approx))
+    assert min(Fs[math.pi / 2]) > 1 - 1e-12
+    assert abs(np.mean(Fs[math.pi / 3]) - 0.875) < 0.06, Fs[math.pi / 3]
