@@ -163,6 +163,9 @@ tn_status tn_plan(tn_ctx* ctx, const tn_slicing* slicing, int64_t max_tensor_siz
             return fail(ctx, TN_EINVAL, "n_sliced smaller than the number of forced wires");
         if (opt.n_sliced > 62) return fail(ctx, TN_EINVAL, "n_sliced must be <= 62");
     }
+    if (slicing && slicing->companions)
+        for (const tnb::CompanionPair& cp : tnb::companion_pairs(ctx->net))
+            opt.companions.push_back({cp.sliced_edge, cp.companion_edge});
     tnb::Plan plan;
     std::string e = tnb::find_plan(ctx->net, ctx->leaves, ctx->req, opt, plan);
     if (!e.empty()) return fail(ctx, TN_EINFEASIBLE, e);

@@ -257,6 +257,42 @@ std::string build_network(const tn_circuit* c, Network& net, const std::vector<i
     return "";
 }
 
+namespace {
+int leg_pos(const HTensor& t, int e) { return (int)(std::find(t.legs.begin(), t.legs.end(), e) - t.legs.begin()); }
+
+bool unitary(const cd P[2][2]) {
+    double dev = 0;
+    for (int r = 0; r < 2; r++)
+        for (int cc = 0; cc < 2; cc++) {
+            cd x = 0;
+            for (int k = 0; k < 2; k++) x += std::conj(P[k][r]) * P[k][cc];
+            dev += std::abs(x - (r == cc ? 1.0 : 0.0));
+        }
+    return dev <= 1e-9;
+}
+}  // namespace
+
+std::vector<CompanionPair> companion_pairs(const Network& net) {
+    std::vector<CompanionPair> out;
+    for (int f = 0; f < (int)net.fsims.size(); f++) {
+        const FsimRec& R = net.fsims[f];
+        for (int side = 0; side < 2; side++) {
+            const int w = R.in[1 - side];  // companion: the other qubit's input edge of the same gate
+            if (w < 0 || R.out[side] < 0) continue;
+            const Edge& E = net.edges[w];
+            if (E.output || E.t0 < 0 || E.t1 < 0 || !net.tensors[E.t0].alive || !net.tensors[E.t1].alive) continue;
+            if (E.t0 == E.t1) continue;
+            if (leg_pos(net.tensors[E.t0], w) >= (int)net.tensors[E.t0].legs.size() ||
+                leg_pos(net.tensors[E.t1], w) >= (int)net.tensors[E.t1].legs.size())
+                continue;
+            // only a unitary P moves across the edge exactly (a drilled hole upstream makes it singular)
+            if (!unitary(R.P[1 - side])) continue;
+            out.push_back({R.out[side], w, f, 1 - side});
+        }
+    }
+    return out;
+}
+
 void add_companions(Network& net, Plan& plan) {
     plan.tied.clear();
     plan.tied_factor.clear();
@@ -264,45 +300,29 @@ void add_companions(Network& net, Plan& plan) {
     std::map<int, int> sliced_bit;
     for (int i = 0; i < (int)plan.sliced.size(); i++) sliced_bit[plan.sliced[i]] = i;
     std::set<int> taken(plan.sliced.begin(), plan.sliced.end());
-    auto leg_pos = [](const HTensor& t, int e) {
-        return (int)(std::find(t.legs.begin(), t.legs.end(), e) - t.legs.begin());
-    };
-    for (const FsimRec& R : net.fsims)
-        for (int side = 0; side < 2; side++) {
-            auto it = sliced_bit.find(R.out[side]);
-            if (it == sliced_bit.end()) continue;
-            const int w = R.in[1 - side];  // companion: the other qubit's input edge of the same gate
-            if (w < 0 || taken.count(w)) continue;
-            Edge& E = net.edges[w];
-            if (E.output || E.t0 < 0 || E.t1 < 0 || !net.tensors[E.t0].alive || !net.tensors[E.t1].alive) continue;
-            HTensor& up = net.tensors[E.t0];
-            HTensor& down = net.tensors[E.t1];
-            const int pu = leg_pos(up, w), pd = leg_pos(down, w);
-            if (pu >= (int)up.legs.size() || pd >= (int)down.legs.size()) continue;
-            Mat2 U, Uc;
-            for (int r = 0; r < 2; r++)
-                for (int cc = 0; cc < 2; cc++) {
-                    U.m[r][cc] = R.P[1 - side][r][cc];
-                    Uc.m[r][cc] = std::conj(R.P[1 - side][r][cc]);
-                }
-            // only a unitary P moves across the edge exactly (a drilled hole upstream makes it singular)
-            double dev = 0;
-            for (int r = 0; r < 2; r++)
-                for (int cc = 0; cc < 2; cc++) {
-                    cd x = 0;
-                    for (int k = 0; k < 2; k++) x += std::conj(U.m[k][r]) * U.m[k][cc];
-                    dev += std::abs(x - (r == cc ? 1.0 : 0.0));
-                }
-            if (dev > 1e-9) continue;
-            // edge index y := fSim input: up'[y] = sum_i P[y][i] up[i], down'[y] = sum_i conj(P[y][i]) down[i]
-            apply_on_leg(up, pu, U);
-            apply_on_leg(down, pd, Uc);
-            taken.insert(w);
-            plan.tied.push_back({w, it->second});
-            plan.tied_wire.push_back({R.q[1 - side], R.kin[1 - side]});
-            const double s2 = std::sin(R.theta) * std::sin(R.theta);
-            plan.tied_factor.push_back((1.0 + s2) / 2.0);
-        }
+    for (const CompanionPair& cp : companion_pairs(net)) {
+        auto it = sliced_bit.find(cp.sliced_edge);
+        if (it == sliced_bit.end() || taken.count(cp.companion_edge)) continue;
+        const FsimRec& R = net.fsims[cp.fsim];
+        const int w = cp.companion_edge, side = cp.side;
+        Edge& E = net.edges[w];
+        HTensor& up = net.tensors[E.t0];
+        HTensor& down = net.tensors[E.t1];
+        Mat2 U, Uc;
+        for (int r = 0; r < 2; r++)
+            for (int cc = 0; cc < 2; cc++) {
+                U.m[r][cc] = R.P[side][r][cc];
+                Uc.m[r][cc] = std::conj(R.P[side][r][cc]);
+            }
+        // edge index y := fSim input: up'[y] = sum_i P[y][i] up[i], down'[y] = sum_i conj(P[y][i]) down[i]
+        apply_on_leg(up, leg_pos(up, w), U);
+        apply_on_leg(down, leg_pos(down, w), Uc);
+        taken.insert(w);
+        plan.tied.push_back({w, it->second});
+        plan.tied_wire.push_back({R.q[side], R.kin[side]});
+        const double s2 = std::sin(R.theta) * std::sin(R.theta);
+        plan.tied_factor.push_back((1.0 + s2) / 2.0);
+    }
 }
 
 void simplify(Network& net) {

@@ -125,9 +125,21 @@ struct Ctx {
     double max_elems;
 };
 
-double node_size(const Node& n, const Bits& S) { return n.rows * std::ldexp(1.0, popc_andnot(n.legs, S)); }
+// companion edges (tn_slicing.companions): slicing an edge also cuts its companion, so every cost below is
+// evaluated on the closure of the planner's sliced set (companions of companions are not cut)
+thread_local const std::vector<std::pair<int, int>>* g_companions = nullptr;
+inline Bits closure(const Bits& S) {
+    if (!g_companions || g_companions->empty()) return S;
+    Bits r = S;
+    for (const auto& p : *g_companions)
+        if (S.get(p.first)) r.set(p.second);
+    return r;
+}
 
-StepCost node_step(const Tree& t, int v, const Bits& S) {
+double node_size_raw(const Node& n, const Bits& C) { return n.rows * std::ldexp(1.0, popc_andnot(n.legs, C)); }
+double node_size(const Node& n, const Bits& S) { return node_size_raw(n, closure(S)); }
+
+StepCost node_step_raw(const Tree& t, int v, const Bits& S) {
     const Node& N = t.nodes[v];
     const Node& A = t.nodes[N.left];
     const Node& B = t.nodes[N.right];
@@ -135,6 +147,7 @@ StepCost node_step(const Tree& t, int v, const Bits& S) {
     const int u = popc_andnot(A.legs | B.legs, S);
     return step_cost(a, b, c, u, A.rows, B.rows, N.rows, A.q != 0, B.q != 0);
 }
+StepCost node_step(const Tree& t, int v, const Bits& S) { return node_step_raw(t, v, closure(S)); }
 
 struct TreeEval {
     double time = 0, cmac = 0, bytes = 0, peak = 0;
@@ -142,11 +155,12 @@ struct TreeEval {
 
 TreeEval eval_tree(const Tree& t, const Bits& S) {
     TreeEval e;
+    const Bits C = closure(S);
     for (int v = 0; v < (int)t.nodes.size(); v++) {
         const Node& N = t.nodes[v];
-        e.peak = std::max(e.peak, node_size(N, S));
+        e.peak = std::max(e.peak, node_size_raw(N, C));
         if (N.leaf >= 0) continue;
-        StepCost s = node_step(t, v, S);
+        StepCost s = node_step_raw(t, v, C);
         e.time += s.time;
         e.cmac += s.cmac;
         e.bytes += s.bytes;
@@ -194,7 +208,7 @@ bool reconf_node(Tree& t, int v, Ctx& cx) {
     std::unordered_map<int, int> loc;
     std::vector<LBits> fl(K);
     for (int i = 0; i < K; i++) {
-        Bits eff = andnot(t.nodes[front[i]].legs, cx.sliced);
+        Bits eff = andnot(t.nodes[front[i]].legs, closure(cx.sliced));
         for (int wd = 0; wd < W; wd++) {
             uint64_t m = eff.w[wd];
             while (m) {
@@ -603,6 +617,10 @@ std::string find_plan(const Network& net, const std::vector<Leaf>& leaves, const
         return "";
     }
 
+    struct CompGuard {
+        explicit CompGuard(const std::vector<std::pair<int, int>>* c) { g_companions = c; }
+        ~CompGuard() { g_companions = nullptr; }
+    } comp_guard(&opt.companions);
     std::mt19937_64 rng(opt.seed ? opt.seed : 1);
     const int trials = opt.trials > 0 ? opt.trials : 24;
     const double budget = opt.time_budget_s > 0 ? opt.time_budget_s : 30.0;
@@ -656,8 +674,8 @@ std::string find_plan(const Network& net, const std::vector<Leaf>& leaves, const
             const double thr = ev.peak > opt.max_elems ? opt.max_elems : ev.peak * 0.999;
             for (const Node& N : pt.second.nodes)
                 if (node_size(N, S) > thr) cand = cand | N.legs;
-            cand = andnot(cand & internal_bits, S);
-            if (ev.peak <= opt.max_elems) cand = andnot(internal_bits, S);
+            cand = andnot(cand & internal_bits, closure(S));
+            if (ev.peak <= opt.max_elems) cand = andnot(internal_bits, closure(S));
             int be = -1;
             double bt = 1e300;
             for (int e : internal) {
@@ -708,8 +726,8 @@ std::string find_plan(const Network& net, const std::vector<Leaf>& leaves, const
             Bits cand;
             for (const Node& N : t.nodes)
                 if (node_size(N, cx.sliced) > thr) cand = cand | N.legs;
-            cand = andnot(cand & internal_bits, cx.sliced);
-            if (!need_peak) cand = andnot(internal_bits, cx.sliced);  // only the count is missing
+            cand = andnot(cand & internal_bits, closure(cx.sliced));
+            if (!need_peak) cand = andnot(internal_bits, closure(cx.sliced));  // only the count is missing
             int be = -1;
             double bt = 1e300, bpeak = 1e300;
             for (int e : internal) {

@@ -109,8 +109,15 @@ struct Plan {
 // `net` (pass a copy) and fills plan.tied / plan.tied_factor ((1 + sin^2 theta)/2 each).
 void add_companions(Network& net, Plan& plan);
 
+// (sliced edge -> companion edge) pairs that add_companions would cut, for the planner's cost model
+struct CompanionPair {
+    int sliced_edge, companion_edge, fsim, side;  // side: which input of net.fsims[fsim] is the companion
+};
+std::vector<CompanionPair> companion_pairs(const Network& net);
+
 struct PlanOptions {
     int n_sliced = -1;
+    std::vector<std::pair<int, int>> companions;  // (edge, companion): slicing edge also cuts companion
     std::vector<int> forced;   // edge ids
     uint64_t seed = 1;
     int trials = 0;
