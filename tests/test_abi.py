@@ -282,3 +282,33 @@ def test_drilled_holes_shrink_the_network(T):
         with pytest.raises(T.TnError) as e:
             T.SparseState(circ, c.bitstrings(n), c.open_mask(n), holes=bad)
         assert e.value.status == T.TN_EINVAL
+
+
+def test_companion_plan_report(T):
+    """tn_slicing.companions: every companion is the oracle's companion of its tied sliced wire (the other
+    input of the fSim that ends that wire) and companion_fidelity = prod (1 + sin^2 theta_i)/2 over those
+    gates, with theta read from the circuit."""
+    import math
+    from oracle import sv
+    c = configs.get(3)
+    circ = c.circuit()
+    n = circ["n"]
+    ss = T.SparseState(circ, c.bitstrings(n), c.open_mask(n))
+    info = ss.plan(1 << c.log2_tmax, n_sliced=c.n_sliced, seed=3, trials=8, time_budget_s=300, companions=True)
+    wires = info["sliced_wires"]
+    assert info["companions"]
+    flat = [g for m in circ["moments"] for g in m]
+    want = 1.0
+    for (q, k, i) in info["companions"]:
+        assert 0 <= i < info["s"]
+        assert sv.companion_of(circ, wires[i]) == (q, k)
+        # the gate: the (k+1)-th gate on q
+        seen, theta = 0, None
+        for g in flat:
+            if (g["target"] == q if g["type"] == "single" else q in g["targets"]):
+                seen += 1
+                if seen == k + 1:
+                    theta = g["theta"]
+                    break
+        want *= (1 + math.sin(theta) ** 2) / 2
+    assert abs(info["companion_fidelity"] - want) < 1e-12
