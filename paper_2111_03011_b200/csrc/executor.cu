@@ -279,9 +279,9 @@ int set_smem_attrs(std::string& err) {
     return TN_OK;
 }
 
-// GEMM tile shape: CTA pairs (256 x 256 tiles) when D has at least 256 rows and, for plain GEMMs, 256
-// columns (grouped tiles bound N per tile); single-CTA 128 x {128, 64, 32} tiles otherwise.
-void pick_gemm_tile(int64_t Dm, int64_t Dn, bool grouped, int& bn, int& cg) {
+// GEMM tile shape: CTA pairs (256 x 256 tiles) when D has at least 256 rows, K2 > 128 and, for plain GEMMs,
+// 256 columns (grouped tiles bound N per tile); single-CTA 128 x {128, 64, 32} tiles otherwise.
+void pick_gemm_tile(int64_t Dm, int64_t Dn, int64_t K2, bool grouped, int& bn, int& cg) {
     cg = 1;
     bn = Dn >= 128 ? 128 : (Dn >= 64 ? 64 : 32);
     if (grouped) {
@@ -292,7 +292,10 @@ void pick_gemm_tile(int64_t Dm, int64_t Dn, bool grouped, int& bn, int& cg) {
         }
         return;
     }
-    if (Dm >= 256 && Dn >= 256) {  // measured: pairs lose at Dn = 128 (config 3 steps 64, 85)
+    // measured (config 3): pairs lose at Dn = 128 and for short K (K2 <= 128: a pair tile is only 4 k-blocks,
+    // so the smaller single-CTA tiles overlap their fill and epilogue better)
+    if (K2 <= 128) return;
+    if (Dm >= 256 && Dn >= 256) {
         cg = 2;
         bn = 256;
     }
@@ -343,7 +346,7 @@ void launch_gemm(const Launch& L, cudaStream_t st) {
 // fills the GEMM fields of L for D = X Y^T, X [Dm][K2], Y [Dn][K2] (tile shape, tensor maps, grid)
 bool setup_gemm(Launch& L, const void* ahi, const void* alo, const void* bhi, const void* blo, int64_t Dm,
                 int64_t Dn, int64_t K2, bool grouped) {
-    pick_gemm_tile(Dm, Dn, grouped, L.gBN, L.gCG);
+    pick_gemm_tile(Dm, Dn, K2, grouped, L.gBN, L.gCG);
     const int bh = L.gBN / L.gCG;
     if (!make_map(&L.tm[0], ahi, Dm, K2) || !make_map(&L.tm[1], alo, Dm, K2) || !make_map(&L.tm[2], bhi, Dn, K2, bh) ||
         !make_map(&L.tm[3], blo, Dn, K2, bh))
