@@ -85,6 +85,8 @@ struct Launch {
     int ni = 0, team = 1;
     int rows_mode = 0;  // k_apply_rows (row-staged gather-contract)
     int na = 0;         // k_apply_na: orbits per thread = 2^na
+    int nob = -1;       // orbit bits (<= 8) with per-bit offsets, for k_chain (-1: not available)
+    uint32_t ob_c[8] = {0}, ob_a[8] = {0}, ob_b[8] = {0};
     int rg = 0, rg_fat = 0, rg_fb = 0;  // k_apply_rg<FAT, FB> (row GEMM)
     kern::RowGemmDev rgp;
     kern::PrepADev pa;
@@ -401,7 +403,8 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
     // chaining up to 8192 in one CTA, were both slower on config 3)
     constexpr int64_t fuse_max = 256;
     auto small = [&](const Launch& L) {
-        return L.kind == K_APPLY && L.ap.ktab != nullptr && L.ap.R * L.ap.n_orbits <= fuse_max && L.cmac <= 4.0e6 &&
+        return L.kind == K_APPLY && L.ap.ktab != nullptr && L.nob >= 0 && L.ap.nk <= 12 &&
+               L.ap.R * L.ap.n_orbits <= fuse_max && L.cmac <= 4.0e6 &&
                !L.ap.stage_b && !L.rows_mode && !L.na && !L.rg;
     };
     auto ov = [](const void* a, int64_t na, const void* b, int64_t nb) {
@@ -437,6 +440,16 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
             m.ntab = L.ap.ntab;
             m.nk = L.ap.nk;
             m.ni = L.ni;
+            m.nob = L.nob;
+            for (int t = 0; t < 8; t++) {
+                m.ob_c[t] = L.ob_c[t];
+                m.ob_a[t] = L.ob_a[t];
+                m.ob_b[t] = L.ob_b[t];
+            }
+            for (int t = 0; t < L.ap.nk && t < 12; t++) {
+                m.kb_a[t] = 1u << L.ap.kA[t];
+                m.kb_b[t] = 1u << L.ap.kB[t];
+            }
             for (int t = 0; t < 16; t++) {
                 m.inner_c[t] = L.ap.inner_c[t];
                 m.inner_b[t] = L.ap.inner_b[t];
@@ -675,6 +688,14 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
             }
             const int nob = (int)orb.size();
             p.n_orbits = (int64_t)1 << nob;
+            if (nob <= 8 && !L.na) {
+                L.nob = nob;
+                for (int t = 0; t < nob; t++) {
+                    L.ob_c[t] = 1u << orb[t];
+                    L.ob_a[t] = a_of_c[orb[t]] >= 0 ? 1u << a_of_c[orb[t]] : 0u;
+                    L.ob_b[t] = b_of_c[orb[t]] >= 0 ? 1u << b_of_c[orb[t]] : 0u;
+                }
+            }
             p.ntab = (nob + 7) / 8;
             for (int ii = 0; ii < (1 << a.n_inner); ii++) {
                 uint32_t co = 0, bo = 0;

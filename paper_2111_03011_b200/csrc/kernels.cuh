@@ -329,24 +329,29 @@ struct MStep {
     int64_t a_row, b_row, c_row, n_orbits, total;
     const uint32_t* tab;
     const uint32_t* ktab;
-    int ntab, nk, ni, ndep, barrier, pad;  // barrier: k_chain syncs the CTA before this step
+    int ntab, nk, ni, ndep, barrier, nob;  // barrier: k_chain syncs the CTA before this step
     int dep[MULTI_MAX_DEPS];
     uint32_t inner_c[16], inner_b[16];
+    // per-bit offsets (no table lookups on the chain's critical path): orbit bit t -> (C, A, B) offsets,
+    // contracted bit t -> (A, B) offsets
+    uint32_t ob_c[8], ob_a[8], ob_b[8];
+    uint32_t kb_a[12], kb_b[12];
 };
 
-// one work item (output orbit w) of a fused tiny step
+// one work item (output orbit w) of a fused tiny step: offsets from per-bit sums (XOR of disjoint bits)
+// instead of table lookups on the chain's critical path
 __device__ __forceinline__ void multi_item(const MStep& S, int64_t w) {
-    const int64_t r = w / S.n_orbits;
-    const int64_t o = w - r * S.n_orbits;
-    uint32_t coff = 0, aoff = 0, boff = 0;
-    for (int t = 0; t < S.ntab; t++) {
-        const uint4 e = __ldg(((const uint4*)S.tab) + (t << 8) + (int)((o >> (8 * t)) & 255));
-        coff += e.x;
-        aoff += e.y;
-        boff += e.z;
-    }
+    const int64_t r = w >> S.nob;
+    const uint32_t o = (uint32_t)(w & ((1 << S.nob) - 1));
     const int64_t ra = S.ma ? (int64_t)__ldg(S.ma + r) : r;
     const int64_t rb = S.mb ? (int64_t)__ldg(S.mb + r) : 0;
+    uint32_t coff = 0, aoff = 0, boff = 0;
+    for (int t = 0; t < S.nob; t++)
+        if ((o >> t) & 1) {
+            coff ^= S.ob_c[t];
+            aoff ^= S.ob_a[t];
+            boff ^= S.ob_b[t];
+        }
     const float2* Ar = S.A + ra * S.a_row + aoff;
     const float2* Br = S.B + rb * S.b_row + boff;
     const int nout = 1 << S.ni;
@@ -355,12 +360,19 @@ __device__ __forceinline__ void multi_item(const MStep& S, int64_t w) {
 #pragma unroll
     for (int ii = 0; ii < 16; ii++) acc[ii] = make_float2(0.f, 0.f);
 #pragma unroll 4
-    for (int64_t kk = 0; kk < K; kk++) {
-        const uint2 kab = __ldg(((const uint2*)S.ktab) + kk);
-        const float2 a = __ldcg(Ar + kab.x);
+    for (int64_t i = 0; i < K; i++) {
+        // offsets of contraction index i from its bits: independent across iterations, so the unrolled
+        // loads of several iterations are in flight together
+        uint32_t ka = 0, kb = 0;
+        for (int t = 0; t < S.nk; t++)
+            if ((i >> t) & 1) {
+                ka ^= S.kb_a[t];
+                kb ^= S.kb_b[t];
+            }
+        const float2 a = __ldcg(Ar + ka);
 #pragma unroll
         for (int ii = 0; ii < 16; ii++)
-            if (ii < nout) acc[ii] = cmac(acc[ii], a, __ldcg(Br + kab.y + S.inner_b[ii]));
+            if (ii < nout) acc[ii] = cmac(acc[ii], a, __ldcg(Br + kb + S.inner_b[ii]));
     }
     float2* Cr = S.C + r * S.c_row + coff;
 #pragma unroll
@@ -368,8 +380,9 @@ __device__ __forceinline__ void multi_item(const MStep& S, int64_t w) {
         if (ii < nout) __stcg(Cr + S.inner_c[ii], acc[ii]);
 }
 
-// a __syncthreads only before a step that depends on a step issued since the previous barrier (S.barrier,
-// host-computed from the run's hazards), so independent neighbours overlap.
+// A run of tiny steps (<= 256 work items each) executed by ONE CTA in program order: no cross-CTA
+// synchronisation; a __syncthreads only before a step that depends on a step issued since the previous
+// barrier (S.barrier, host-computed from the run's hazards), so independent neighbours overlap.
 __global__ void __launch_bounds__(256) k_chain(const MStep* __restrict__ steps, int nsteps) {
     // the run's descriptors live in smem: the item loop reads table pointers / offsets with LDS, not with a
     // chain of dependent global loads per output
