@@ -435,9 +435,6 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
             m.c_row = L.ap.c_row;
             m.n_orbits = L.ap.n_orbits;
             m.total = L.ap.R * L.ap.n_orbits;
-            m.tab = L.ap.tab;
-            m.ktab = L.ap.ktab;
-            m.ntab = L.ap.ntab;
             m.nk = L.ap.nk;
             m.ni = L.ni;
             m.nob = L.nob;

@@ -327,9 +327,7 @@ struct MStep {
     const int32_t* ma;
     const int32_t* mb;
     int64_t a_row, b_row, c_row, n_orbits, total;
-    const uint32_t* tab;
-    const uint32_t* ktab;
-    int ntab, nk, ni, ndep, barrier, nob;  // barrier: k_chain syncs the CTA before this step
+    int nk, ni, ndep, barrier, nob, pad;  // barrier: k_chain syncs the CTA before this step
     int dep[MULTI_MAX_DEPS];
     uint32_t inner_c[16], inner_b[16];
     // per-bit offsets (no table lookups on the chain's critical path): orbit bit t -> (C, A, B) offsets,
