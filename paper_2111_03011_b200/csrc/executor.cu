@@ -268,6 +268,7 @@ int set_smem_attrs(std::string& err) {
                                          kern::ROWS_SMEM_MAX))
     SETR(0); SETR(1); SETR(2); SETR(3); SETR(4);
 #undef SETR
+    CK(cudaFuncSetAttribute(kern::k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, kern::CHAIN_SMEM_MAX));
     CK(set_rg_attrs_fb<0>()); CK(set_rg_attrs_fb<1>()); CK(set_rg_attrs_fb<2>());
     CK(set_rg_attrs_fb<3>()); CK(set_rg_attrs_fb<4>()); CK(set_rg_attrs_fb<5>());
     CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Cfg<128>::SMEM));
@@ -391,7 +392,7 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
             kern::k_readout<<<L.grid, L.block, 0, st>>>(L.F, L.ridx, P.acc, L.M, P.counter);
             break;
         case K_MULTI:
-            kern::k_chain<<<1, 256, 0, st>>>(P.msteps + L.m_first, L.m_n);
+            kern::k_chain<<<1, 256, L.smem, st>>>(P.msteps + L.m_first, L.m_n);
             break;
     }
 }
@@ -494,6 +495,47 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
         M.m_n = (int)run.size();
         M.rows = (int64_t)run.size();
         M.block = dim3(256);
+        // run-internal intermediates in shared memory: a step's output that no launch after the run reads
+        // (by workspace range) lives in k_chain's smem; consumers in the run find it by base pointer (the
+        // latest producer in program order)
+        {
+            int64_t top = 0;  // float2 units
+            std::vector<int64_t> c_sm(run.size(), -1);
+            for (size_t t = 0; t < run.size(); t++) {
+                run[t].a_sm = run[t].b_sm = run[t].c_sm = -1;
+                const Launch& L = in[i + t];
+                const int64_t cb = L.c_bytes;
+                if (cb > 64 * 1024 || (top * 8 + cb) > kern::CHAIN_SMEM_MAX) continue;
+                const MemAcc* w = nullptr;
+                for (const MemAcc& x : L.mem)
+                    if (x.write) w = &x;
+                // only per-slice workspace: persistent (prologue) results are read by the slice graphs
+                if (!w || w->region != REG_WORK) continue;
+                bool ext = false;
+                for (size_t u = j; u < in.size() && !ext; u++)
+                    for (const MemAcc& x : in[u].mem)
+                        if (!x.write && x.region == w->region && x.offset < w->offset + w->bytes &&
+                            w->offset < x.offset + x.bytes)
+                            ext = true;
+                if (ext) continue;
+                c_sm[t] = top;
+                top += ((cb / 8) + 15) & ~(int64_t)15;
+            }
+            for (size_t t = 0; t < run.size(); t++) {
+                run[t].c_sm = (int)c_sm[t];
+                for (int t2 = (int)t - 1; t2 >= 0; t2--)
+                    if (run[t2].C == run[t].A) {
+                        run[t].a_sm = (int)c_sm[t2];
+                        break;
+                    }
+                for (int t2 = (int)t - 1; t2 >= 0; t2--)
+                    if (run[t2].C == run[t].B) {
+                        run[t].b_sm = (int)c_sm[t2];
+                        break;
+                    }
+            }
+            M.smem = (size_t)top * 8;
+        }
         // one CTA runs the chain in program order (k_chain); a barrier goes before a step that depends on
         // one issued since the previous barrier
         {

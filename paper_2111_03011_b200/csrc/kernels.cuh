@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(256) k_apply_rows(const ApplyDev p) {
 // st.global.cg because the run reuses workspace buffers.
 constexpr int MULTI_MAX_DEPS = 8;
 constexpr int CHAIN_MAX_STEPS = 64;    // steps per k_chain launch (descriptors staged in smem)
+constexpr int CHAIN_SMEM_MAX = 160 * 1024;  // run-internal intermediates kept in k_chain's shared memory
 struct MStep {
     const float2* A;
     const float2* B;
@@ -327,7 +328,8 @@ struct MStep {
     const int32_t* ma;
     const int32_t* mb;
     int64_t a_row, b_row, c_row, n_orbits, total;
-    int nk, ni, ndep, barrier, nob, pad;  // barrier: k_chain syncs the CTA before this step
+    int nk, ni, ndep, barrier, nob;  // barrier: k_chain syncs the CTA before this step
+    int a_sm, b_sm, c_sm;            // >= 0: the operand lives in the chain's shared memory at this float2 offset
     int dep[MULTI_MAX_DEPS];
     uint32_t inner_c[16], inner_b[16];
     // per-bit offsets (no table lookups on the chain's critical path): orbit bit t -> (C, A, B) offsets,
@@ -338,7 +340,7 @@ struct MStep {
 
 // one work item (output orbit w) of a fused tiny step: offsets from per-bit sums (XOR of disjoint bits)
 // instead of table lookups on the chain's critical path
-__device__ __forceinline__ void multi_item(const MStep& S, int64_t w) {
+__device__ __forceinline__ void multi_item(const MStep& S, int64_t w, float2* sm) {
     const int64_t r = w >> S.nob;
     const uint32_t o = (uint32_t)(w & ((1 << S.nob) - 1));
     const int64_t ra = S.ma ? (int64_t)__ldg(S.ma + r) : r;
@@ -350,8 +352,9 @@ __device__ __forceinline__ void multi_item(const MStep& S, int64_t w) {
             aoff ^= S.ob_a[t];
             boff ^= S.ob_b[t];
         }
-    const float2* Ar = S.A + ra * S.a_row + aoff;
-    const float2* Br = S.B + rb * S.b_row + boff;
+    const bool a_sm = S.a_sm >= 0, b_sm = S.b_sm >= 0;  // uniform per step
+    const float2* Ar = (a_sm ? sm + S.a_sm : S.A) + ra * S.a_row + aoff;
+    const float2* Br = (b_sm ? sm + S.b_sm : S.B) + rb * S.b_row + boff;
     const int nout = 1 << S.ni;
     const int64_t K = (int64_t)1 << S.nk;
     float2 acc[16];
@@ -367,15 +370,24 @@ __device__ __forceinline__ void multi_item(const MStep& S, int64_t w) {
                 ka ^= S.kb_a[t];
                 kb ^= S.kb_b[t];
             }
-        const float2 a = __ldcg(Ar + ka);
+        const float2 a = a_sm ? Ar[ka] : __ldcg(Ar + ka);
 #pragma unroll
         for (int ii = 0; ii < 16; ii++)
-            if (ii < nout) acc[ii] = cmac(acc[ii], a, __ldcg(Br + kb + S.inner_b[ii]));
+            if (ii < nout) {
+                const float2* bp = Br + kb + S.inner_b[ii];
+                acc[ii] = cmac(acc[ii], a, b_sm ? *bp : __ldcg(bp));
+            }
     }
-    float2* Cr = S.C + r * S.c_row + coff;
+    const bool c_sm = S.c_sm >= 0;
+    float2* Cr = (c_sm ? sm + S.c_sm : S.C) + r * S.c_row + coff;
 #pragma unroll
     for (int ii = 0; ii < 16; ii++)
-        if (ii < nout) __stcg(Cr + S.inner_c[ii], acc[ii]);
+        if (ii < nout) {
+            if (c_sm)
+                Cr[S.inner_c[ii]] = acc[ii];
+            else
+                __stcg(Cr + S.inner_c[ii], acc[ii]);
+        }
 }
 
 // A run of tiny steps (<= 256 work items each) executed by ONE CTA in program order: no cross-CTA
@@ -385,6 +397,7 @@ __global__ void __launch_bounds__(256) k_chain(const MStep* __restrict__ steps, 
     // the run's descriptors live in smem: the item loop reads table pointers / offsets with LDS, not with a
     // chain of dependent global loads per output
     __shared__ MStep sS[CHAIN_MAX_STEPS];
+    extern __shared__ float2 chain_sm[];  // run-internal intermediates (host-assigned offsets)
     {
         const int words = nsteps * (int)(sizeof(MStep) / 4);
         const uint32_t* src = (const uint32_t*)steps;
@@ -395,7 +408,7 @@ __global__ void __launch_bounds__(256) k_chain(const MStep* __restrict__ steps, 
     for (int s = 0; s < nsteps; s++) {
         const MStep& S = sS[s];
         if (S.barrier) __syncthreads();
-        for (int64_t w = threadIdx.x; w < S.total; w += 256) multi_item(S, w);
+        for (int64_t w = threadIdx.x; w < S.total; w += 256) multi_item(S, w, chain_sm);
     }
 }
 
