@@ -70,7 +70,7 @@ CONFIGS = {
     2: Config(2, "20q-m8", "rect:4x5", 8, SUPREMACY, L=64, n_open=6, n_sliced=4, log2_tmax=20,
               note="2^4 slices all contracted"),
     3: Config(3, "30q-m12", "rect:5x6", 12, SUPREMACY, L=1024, n_open=6, n_sliced=8, log2_tmax=28,
-              note="2^8 slices, fraction sweep", plan_seed=37, plan_trials=96, plan_budget_s=120.0),
+              note="2^8 slices, fraction sweep", plan_seed=53, plan_trials=96, plan_budget_s=120.0),
     4: Config(4, "53q-m14", "sycamore53", 14, SUPREMACY, L=1 << 14, n_open=6, n_sliced=12, log2_tmax=32,
               open_qubits=[11, 19, 28, 29, 37, 44], note="2^12 slices over 1/2/4/8 GPUs"),
     5: Config(5, "53q-m20", "sycamore53", 20, SUPREMACY, L=1 << 20, n_open=6, n_sliced=-1, log2_tmax=32,
