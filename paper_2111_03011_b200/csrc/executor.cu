@@ -511,12 +511,20 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
                     if (x.write) w = &x;
                 // only per-slice workspace: persistent (prologue) results are read by the slice graphs
                 if (!w || w->region != REG_WORK) continue;
-                bool ext = false;
-                for (size_t u = j; u < in.size() && !ext; u++)
+                // live after the run: some later launch reads the range before a later write covers all of it
+                // (within a launch the reads come first); partial overwrites keep it live (conservative)
+                bool ext = false, dead = false;
+                for (size_t u = j; u < in.size() && !ext && !dead; u++) {
                     for (const MemAcc& x : in[u].mem)
                         if (!x.write && x.region == w->region && x.offset < w->offset + w->bytes &&
                             w->offset < x.offset + x.bytes)
                             ext = true;
+                    if (ext) break;
+                    for (const MemAcc& x : in[u].mem)
+                        if (x.write && x.region == w->region && x.offset <= w->offset &&
+                            x.offset + x.bytes >= w->offset + w->bytes)
+                            dead = true;
+                }
                 if (ext) continue;
                 c_sm[t] = top;
                 top += ((cb / 8) + 15) & ~(int64_t)15;
