@@ -14,7 +14,7 @@ Pure numpy over all 2^W assignments: only for W <= ~20 internal wires.
 from __future__ import annotations
 
 import math
-from typing import Dict, Sequence, Tuple
+from typing import Dict, Tuple
 
 import numpy as np
 

@@ -6,7 +6,7 @@ Open qubits: configs 1-3 the 6 highest ids; 4-5 the paper's ids [11,19,28,29,37,
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import List, Optional
 
 from . import bitstrings as bs

@@ -5,7 +5,6 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2111_03011_b200 as T  # noqa: E402

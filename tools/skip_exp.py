@@ -1,8 +1,8 @@
 """Throughput of variants with concurrent pipelines: each argument is "VAR=val;VAR2=val" env settings read at
 bind (e.g. TNB_SKIP=k1 drops launch kind 1: outputs are then wrong, timing only)."""
-import os, sys, json
+import os
+import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import torch
 import paper_2111_03011_b200 as T
 from tn_inputs import configs
 cfg = int(os.environ.get("CFG", "3"))
