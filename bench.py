@@ -131,7 +131,7 @@ def run_reference(args, cfg, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "slices/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "cfg": cfg.cfg},
+            "config": workload_config(cfg),
             "cpu_baseline": {"kind": "oracle", "cores": s0["cores"], "value": v, "unit": "slices/s",
                              "sample": s0["sample"]},
             "e2e": {"value": v, "unit": "slices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -139,6 +139,16 @@ def run_reference(args, cfg, rank, world):
 
 
 # ------------------------------------------------------------------------------ our arm
+
+def workload_config(cfg) -> dict:
+    """The workload keys both arms report (the GPU arm adds its run-specific keys)."""
+    n = cfg.circuit()["n"]
+    M = cfg.L << len(cfg.open_ids(n))
+    s = cfg.n_sliced
+    return {"workload": f"config{cfg.cfg}: {cfg.name} ({cfg.layout}, m={cfg.cycles}, M={M}, 2^{s} slices all summed)",
+            "n_qubits": n, "cycles": cfg.cycles, "M": M, "L": cfg.L, "l": 1 << len(cfg.open_ids(n)),
+            "slices": 1 << s, "max_tensor_size": 1 << cfg.log2_tmax}
+
 
 def main():
     ap = argparse.ArgumentParser()
@@ -346,10 +356,7 @@ def main():
             "metric": METRIC, "value": slices_per_s, "unit": "slices/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "c64", "data": "synthetic",
-            "config": {"workload": f"config{cfg.cfg}: {cfg.name} ({cfg.layout}, m={cfg.cycles}, "
-                                   f"M={M}, 2^{s} slices all summed)",
-                       "n_qubits": n, "cycles": cfg.cycles, "M": M, "L": cfg.L, "l": ss.l, "slices": nS,
-                       "max_tensor_size": 1 << cfg.log2_tmax, "parallelism": f"slices/{world}",
+            "config": {**workload_config(cfg), "parallelism": f"slices/{world}",
                        "l2": "flushed (512 MB write) before every timed step; per-slice working set "
                              f"{info['workspace_bytes'] / 2**30:.2f} GiB > L2",
                        "setup_s": {"build": t_build, "plan": t_plan, "bind": t_bind}},
