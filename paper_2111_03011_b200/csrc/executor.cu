@@ -112,6 +112,8 @@ struct Launch {
     // operand extents in bytes (apply), for the tiny-step chains' hazard analysis
     int64_t a_bytes = 0, b_bytes = 0, c_bytes = 0;
     std::vector<MemAcc> mem;     // workspace / persistent ranges read and written (graph dependencies)
+    int a_region = REG_NONE, b_region = REG_NONE;  // apply operands' regions (tiny-step chains' preloads)
+    int64_t a_off = 0, b_off = 0;
     // K_MULTI: a k_chain run of tiny steps
     size_t m_first = 0;          // index into Device::msteps_host
     int m_n = 0;
@@ -531,16 +533,38 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
             }
             for (size_t t = 0; t < run.size(); t++) {
                 run[t].c_sm = (int)c_sm[t];
+                run[t].a_pre = run[t].b_pre = 0;
+                bool a_in = false, b_in = false;  // produced inside the run (by pointer)
                 for (int t2 = (int)t - 1; t2 >= 0; t2--)
                     if (run[t2].C == run[t].A) {
                         run[t].a_sm = (int)c_sm[t2];
+                        a_in = true;
                         break;
                     }
                 for (int t2 = (int)t - 1; t2 >= 0; t2--)
                     if (run[t2].C == run[t].B) {
                         run[t].b_sm = (int)c_sm[t2];
+                        b_in = true;
                         break;
                     }
+                // operands from outside the run (the leaf cone's gate tensors, instantiated sliced leaves,
+                // prologue results) that no step of the run writes: preloaded into smem at kernel start, so a
+                // step's only memory round trips are shared-memory ones
+                const Launch& L = in[i + t];
+                auto preload = [&](bool inside, int region, int64_t off, int64_t bytes, int& slot, int& pre) {
+                    if (inside || bytes > 16 * 1024 || (top * 8 + bytes) > kern::CHAIN_SMEM_MAX) return;
+                    if (region != REG_BANK && region != REG_PERS && region != REG_WORK) return;
+                    if (region != REG_BANK)
+                        for (size_t t2 = 0; t2 < run.size(); t2++)
+                            for (const MemAcc& x : in[i + t2].mem)
+                                if (x.write && x.region == region && x.offset < off + bytes && off < x.offset + x.bytes)
+                                    return;
+                    slot = (int)top;
+                    pre = (int)(bytes / 8);
+                    top += ((bytes / 8) + 15) & ~(int64_t)15;
+                };
+                preload(a_in, L.a_region, L.a_off, L.a_bytes, run[t].a_sm, run[t].a_pre);
+                preload(b_in, L.b_region, L.b_off, L.b_bytes, run[t].b_sm, run[t].b_pre);
             }
             M.smem = (size_t)top * 8;
         }
@@ -684,6 +708,10 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
             p.A = (const float2*)ptr(a.A);
             p.B = (const float2*)ptr(a.B);
             p.C = (float2*)ptr(a.C);
+            L.a_region = a.A.region;
+            L.b_region = a.B.region;
+            L.a_off = a.A.offset;
+            L.b_off = a.B.offset;
             p.ma = (const int32_t*)ptr(a.ma);
             p.mb = (const int32_t*)ptr(a.mb);
             p.R = a.R;

@@ -330,6 +330,7 @@ struct MStep {
     int64_t a_row, b_row, c_row, n_orbits, total;
     int nk, ni, ndep, barrier, nob;  // barrier: k_chain syncs the CTA before this step
     int a_sm, b_sm, c_sm;            // >= 0: the operand lives in the chain's shared memory at this float2 offset
+    int a_pre, b_pre;                // > 0: preload this many elements of A / B from global at kernel start
     int dep[MULTI_MAX_DEPS];
     uint32_t inner_c[16], inner_b[16];
     // per-bit offsets (no table lookups on the chain's critical path): orbit bit t -> (C, A, B) offsets,
@@ -403,6 +404,13 @@ __global__ void __launch_bounds__(256) k_chain(const MStep* __restrict__ steps, 
         const uint32_t* src = (const uint32_t*)steps;
         uint32_t* dst = (uint32_t*)sS;
         for (int i = threadIdx.x; i < words; i += 256) dst[i] = src[i];
+    }
+    __syncthreads();
+    // preload the run's external operands (one memory latency for the whole run)
+    for (int s = 0; s < nsteps; s++) {
+        const MStep& S = sS[s];
+        for (int e = threadIdx.x; e < S.a_pre; e += 256) chain_sm[S.a_sm + e] = __ldcg(S.A + e);
+        for (int e = threadIdx.x; e < S.b_pre; e += 256) chain_sm[S.b_sm + e] = __ldcg(S.B + e);
     }
     __syncthreads();
     for (int s = 0; s < nsteps; s++) {
