@@ -52,8 +52,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         src = os.path.join(CSRC, s)
         obj = os.path.join(BUILD, s + ".o")
         if force or _newer(obj, [src] + hdrs):
+            extra = os.environ.get("TNB_NVCC_FLAGS", "").split()  # diagnostics builds, e.g. -DTNB_CHAIN_CLOCK
             out = _run([NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                        "-Xptxas", "-v", "--expt-relaxed-constexpr", "-c", src, "-o", obj])
+                        "-Xptxas", "-v", "--expt-relaxed-constexpr", *extra, "-c", src, "-o", obj])
             if verbose:
                 print(out)
             with open(os.path.join(BUILD, s + ".ptxas.txt"), "w") as f:

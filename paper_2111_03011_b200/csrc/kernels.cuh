@@ -406,6 +406,10 @@ __global__ void __launch_bounds__(256) k_chain(const MStep* __restrict__ steps, 
         for (int i = threadIdx.x; i < words; i += 256) dst[i] = src[i];
     }
     __syncthreads();
+#ifdef TNB_CHAIN_CLOCK
+    long long t_prev = clock64();
+    if (threadIdx.x == 0) printf("[chain] start nsteps %d\n", nsteps);
+#endif
     // preload the run's external operands (one memory latency for the whole run)
     for (int s = 0; s < nsteps; s++) {
         const MStep& S = sS[s];
@@ -413,9 +417,24 @@ __global__ void __launch_bounds__(256) k_chain(const MStep* __restrict__ steps, 
         for (int e = threadIdx.x; e < S.b_pre; e += 256) chain_sm[S.b_sm + e] = __ldcg(S.B + e);
     }
     __syncthreads();
+#ifdef TNB_CHAIN_CLOCK
+    if (threadIdx.x == 0) {
+        const long long t = clock64();
+        printf("[chain] descriptors+preload %lld cycles\n", t - t_prev);
+        t_prev = t;
+    }
+#endif
     for (int s = 0; s < nsteps; s++) {
         const MStep& S = sS[s];
         if (S.barrier) __syncthreads();
+#ifdef TNB_CHAIN_CLOCK
+        if (threadIdx.x == 0) {
+            const long long t = clock64();
+            printf("[chain] step %d items %lld nk %d ni %d a_sm %d b_sm %d c_sm %d barrier %d: %lld cycles since last\n", s,
+                   (long long)S.total, S.nk, S.ni, S.a_sm, S.b_sm, S.c_sm, S.barrier, t - t_prev);
+            t_prev = t;
+        }
+#endif
         for (int64_t w = threadIdx.x; w < S.total; w += 256) multi_item(S, w, chain_sm);
     }
 }
