@@ -70,8 +70,11 @@ constexpr int STAGE_B_MAX = 4096;  // complex elements of B per row staged in sh
 constexpr int RG_SMEM_MAX = 100 * 1024;   // k_apply_rg: B row (<= 8192 complex) + tables + reduction buffer
 constexpr int ROWS_SMEM_MAX = 112 * 1024;  // k_apply_rows: tables + both parent rows in shared memory (>= 2 CTAs/SM)
 
+#ifndef TNB_APPLY_MINB
+#define TNB_APPLY_MINB 3  // 3 CTAs per SM (<= 80 registers): measured 2544 vs 2385 slices/s with 2
+#endif
 template <int NI, int TEAM>
-__global__ void __launch_bounds__(256) k_apply(const ApplyDev p) {
+__global__ void __launch_bounds__(256, TNB_APPLY_MINB) k_apply(const ApplyDev p) {
     extern __shared__ uint32_t sm[];
     const int tabn = p.ntab * 256 * 4;
     for (int i = threadIdx.x; i < tabn; i += blockDim.x) sm[i] = p.tab[i];
@@ -118,6 +121,8 @@ __global__ void __launch_bounds__(256) k_apply(const ApplyDev p) {
             float2 acc[1 << NI];
 #pragma unroll
             for (int ii = 0; ii < (1 << NI); ii++) acc[ii] = make_float2(0.f, 0.f);
+            // unrolled so several iterations' A loads are in flight (the loop is long-scoreboard bound)
+#pragma unroll 4
             for (int64_t kk = lane; kk < K; kk += TEAM) {
                 const uint32_t ka = sk[2 * kk], kb = sk[2 * kk + 1];
                 const float2 a = Ar[ka];
