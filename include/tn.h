@@ -111,6 +111,18 @@ typedef struct {
                                     of the pinned gate, i.e. onto |v> in G's input basis with v the
                                     sliced wire's value (cutting that companion edge too); fidelity
                                     factor (1 + sin^2 theta)/2 each                      */
+    int32_t method;              /* 0 auto (loop program above 160 tensors), 1 flat slicing (every
+                                    sliced wire is a slice-id bit), 2 loop program: a stem sweep with
+                                    local slices summed inside the program and checkpointed segments
+                                    that reuse the head across slices (the
+                                    head result shared by the tail's local slices).  With 2, n_sliced
+                                    is the minimum number of slice-id (global) bits.               */
+    int32_t max_segments;        /* loop program: at most this many segments (<= 0: 8)             */
+    double persist_budget;       /* loop program: complex elements kept across loop iterations
+                                    (checkpointed stems and accumulators; <= 0: 8 x max_tensor_size) */
+    const char* plan_path;       /* nullable: import the plan saved by tn_plan_save at this path
+                                    instead of searching ("plan file is an explicit,
+                                    replayable artifact"); the search options above are ignored    */
 } tn_slicing;
 
 typedef struct {
@@ -131,10 +143,19 @@ typedef struct {
                                     the fSim, after its single-qubit gates -- with v = slice bit b
                                     (owned by ctx)                                             */
     double companion_fidelity;   /* prod (1 + sin^2 theta_i)/2 over the companions   */
+    int32_t s_local;             /* loop program: local sliced wires, summed inside tn_contract    */
+    const int32_t* local_wires;  /* 2*s_local ints, (q, k) pairs, loop-bit order (owned by ctx)   */
+    int32_t n_segments;          /* loop program segments (1 for flat slicing)                     */
+    double total_cmac;           /* modelled CMAC of a tn_contract over all 2^s slices, with the
+                                    loop program's reuse (flat: 2^s * cmac_per_slice + invariant)  */
+    int64_t persist_bytes;       /* device bytes kept across loop iterations (per pipeline)        */
 } tn_plan_info;
 
 /* tn_plan -- P:L91 (complexity-greedy contraction order), P:L246 (slicing: fix index values so
  * that the space fits the device; the sum over sub-tasks returns the original contraction).
+ * info.s / info.sliced_wires are the slice-id (global) wires that tn_contract's slice ids enumerate;
+ * a loop program's local wires (info.local_wires) are summed inside every slice, so a slice id of a loop
+ * program denotes the sum over all local values (Sigma_v Pi_v = I on those wires).
  * max_tensor_size: bound on every intermediate of one slice, in complex elements (<= 2^60 for planning;
  * tn_bind_device accepts plans whose tensors are <= 2^32 elements).
  * Fills *info (pointers owned by the ctx, valid until the next tn_plan or tn_destroy).
@@ -144,6 +165,13 @@ tn_status tn_plan(tn_ctx* ctx, const tn_slicing* slicing, int64_t max_tensor_siz
 
 /* Write the plan (order, sliced wires, per-step shapes, row tables of sparse tensors) as JSON. */
 tn_status tn_plan_dump(const tn_ctx* ctx, const char* path);
+
+/* tn_plan_save -- write the current plan as a replayable plan file: the
+ * contraction order by tensor id, the sliced wires (q, k) in loop-bit order, the number of global bits
+ * and the loop program's segments.  tn_plan with tn_slicing.plan_path = this file reproduces the plan on
+ * the same circuit and request (a ctx on another rank or process).  EINVAL before tn_plan or when the
+ * file cannot be written. */
+tn_status tn_plan_save(const tn_ctx* ctx, const char* path);
 
 /* tn_bind_device -- uploads leaf bank, row maps and the step program, captures the per-slice
  * CUDA graph.  workspace: device pointer of >= info.workspace_bytes (from the caller's allocator,

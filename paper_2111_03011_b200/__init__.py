@@ -47,7 +47,9 @@ class TnCircuit(ctypes.Structure):
 class TnSlicing(ctypes.Structure):
     _fields_ = [("n_sliced", ctypes.c_int32), ("n_forced", ctypes.c_int32),
                 ("forced_wires", ctypes.POINTER(ctypes.c_int32)), ("seed", ctypes.c_uint64),
-                ("trials", ctypes.c_int32), ("time_budget_s", ctypes.c_double), ("companions", ctypes.c_int32)]
+                ("trials", ctypes.c_int32), ("time_budget_s", ctypes.c_double), ("companions", ctypes.c_int32),
+                ("method", ctypes.c_int32), ("max_segments", ctypes.c_int32), ("persist_budget", ctypes.c_double),
+                ("plan_path", ctypes.c_char_p)]
 
 
 class TnPlanInfo(ctypes.Structure):
@@ -57,7 +59,9 @@ class TnPlanInfo(ctypes.Structure):
                 ("cmac_per_slice", ctypes.c_double), ("bytes_per_slice", ctypes.c_double),
                 ("gemm_cmac_per_slice", ctypes.c_double), ("n_invariant_steps", ctypes.c_int64),
                 ("invariant_cmac", ctypes.c_double), ("n_companions", ctypes.c_int32),
-                ("companion_wires", ctypes.POINTER(ctypes.c_int32)), ("companion_fidelity", ctypes.c_double)]
+                ("companion_wires", ctypes.POINTER(ctypes.c_int32)), ("companion_fidelity", ctypes.c_double),
+                ("s_local", ctypes.c_int32), ("local_wires", ctypes.POINTER(ctypes.c_int32)),
+                ("n_segments", ctypes.c_int32), ("total_cmac", ctypes.c_double), ("persist_bytes", ctypes.c_int64)]
 
 
 class TnLaunchStat(ctypes.Structure):
@@ -71,7 +75,7 @@ class TnReport(ctypes.Structure):
                 ("f", "F_norm", "xeb", "log_xeb", "entropy_samples", "entropy_state", "pt_ks")]
 
 
-EXPORTS = ["tn_build", "tn_build_drilled", "tn_plan", "tn_plan_dump", "tn_bind_device", "tn_contract", "tn_profile_slice",
+EXPORTS = ["tn_build", "tn_build_drilled", "tn_plan", "tn_plan_dump", "tn_plan_save", "tn_bind_device", "tn_contract", "tn_profile_slice",
            "tn_sample", "tn_sample_report", "tn_destroy", "tn_last_error", "tn_version", "tn_debug_gemm_tf32x3",
            "tn_debug_network", "tn_debug_launch_counts"]
 
@@ -93,6 +97,7 @@ def lib():
                                    P(c.c_void_p)]
     L.tn_plan.argtypes = [c.c_void_p, P(TnSlicing), c.c_int64, P(TnPlanInfo)]
     L.tn_plan_dump.argtypes = [c.c_void_p, c.c_char_p]
+    L.tn_plan_save.argtypes = [c.c_void_p, c.c_char_p]
     L.tn_bind_device.argtypes = [c.c_void_p, c.c_int, c.c_void_p, c.c_size_t, c.c_void_p]
     L.tn_contract.argtypes = [c.c_void_p, P(c.c_uint64), c.c_int64, c.c_void_p, c.c_int32, P(c.c_double)]
     L.tn_profile_slice.argtypes = [c.c_void_p, c.c_uint64, P(TnLaunchStat), c.c_int32, P(c.c_int32)]
@@ -109,7 +114,7 @@ def lib():
                                        c.c_int32, c.c_void_p]
     L.tn_debug_network.argtypes = [c.c_void_p, P(c.c_int64), P(c.c_int64), P(c.c_int64)]
     L.tn_debug_launch_counts.argtypes = [c.c_void_p, P(c.c_int64), P(c.c_int64)]
-    for name in ("tn_build", "tn_build_drilled", "tn_plan", "tn_plan_dump", "tn_bind_device", "tn_contract", "tn_profile_slice",
+    for name in ("tn_build", "tn_build_drilled", "tn_plan", "tn_plan_dump", "tn_plan_save", "tn_bind_device", "tn_contract", "tn_profile_slice",
                  "tn_sample", "tn_sample_report", "tn_debug_gemm_tf32x3", "tn_debug_network", "tn_debug_launch_counts"):
         getattr(L, name).restype = c.c_int
     _lib = L
@@ -199,9 +204,13 @@ class SparseState:
 
     # -------------------------------------------------------------- tn_plan
     def plan(self, max_tensor_size: int, n_sliced: int = -1, forced_wires: Sequence = (), seed: int = 1,
-             trials: int = 0, time_budget_s: float = 0.0, companions: bool = False) -> dict:
+             trials: int = 0, time_budget_s: float = 0.0, companions: bool = False, method: int = 0,
+             max_segments: int = 0, persist_budget: float = 0.0, plan_path: Optional[str] = None) -> dict:
+        """tn_plan.  method 0 auto / 1 flat slicing / 2 loop program (local slices + head reuse);
+        plan_path imports a plan file written by save_plan (the search options are then ignored)."""
         fw = (ctypes.c_int32 * max(1, 2 * len(forced_wires)))(*[v for w in forced_wires for v in w])
-        sl = TnSlicing(n_sliced, len(forced_wires), fw, seed, trials, time_budget_s, 1 if companions else 0)
+        sl = TnSlicing(n_sliced, len(forced_wires), fw, seed, trials, time_budget_s, 1 if companions else 0,
+                       method, max_segments, persist_budget, plan_path.encode() if plan_path else None)
         info = TnPlanInfo()
         self._check(lib().tn_plan(self._ctx, ctypes.byref(sl), int(max_tensor_size), ctypes.byref(info)))
         self.info = {
@@ -215,8 +224,15 @@ class SparseState:
             "companions": [(info.companion_wires[3 * i], info.companion_wires[3 * i + 1],
                             info.companion_wires[3 * i + 2]) for i in range(info.n_companions)],
             "companion_fidelity": info.companion_fidelity,
+            "s_local": info.s_local,
+            "local_wires": [(info.local_wires[2 * i], info.local_wires[2 * i + 1]) for i in range(info.s_local)],
+            "n_segments": info.n_segments, "total_cmac": info.total_cmac, "persist_bytes": info.persist_bytes,
         }
         return self.info
+
+    def save_plan(self, path: str):
+        """tn_plan_save: write the current plan as a replayable plan file."""
+        self._check(lib().tn_plan_save(self._ctx, path.encode()))
 
     def dump(self, path: str):
         self._check(lib().tn_plan_dump(self._ctx, path.encode()))

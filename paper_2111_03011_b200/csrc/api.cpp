@@ -20,6 +20,7 @@ struct tn_ctx {
     tnb::Plan plan;
     tnb::Program prog;
     std::vector<int32_t> sliced_wires;
+    std::vector<int32_t> local_wires;
     std::vector<int32_t> companion_wires;
     tn_plan_info info{};
     tnb::Device* dev = nullptr;
@@ -166,9 +167,21 @@ tn_status tn_plan(tn_ctx* ctx, const tn_slicing* slicing, int64_t max_tensor_siz
     if (slicing && slicing->companions)
         for (const tnb::CompanionPair& cp : tnb::companion_pairs(ctx->net))
             opt.companions.push_back({cp.sliced_edge, cp.companion_edge});
+    if (slicing) {
+        opt.method = slicing->method;
+        if (slicing->max_segments > 0) opt.max_segments = slicing->max_segments;
+        opt.persist_budget = slicing->persist_budget;
+    }
     tnb::Plan plan;
-    std::string e = tnb::find_plan(ctx->net, ctx->leaves, ctx->req, opt, plan);
-    if (!e.empty()) return fail(ctx, TN_EINFEASIBLE, e);
+    std::string e;
+    if (slicing && slicing->plan_path) {
+        if (slicing->companions) return fail(ctx, TN_EINVAL, "plan import does not support companion edges");
+        e = tnb::load_plan(ctx->net, ctx->leaves, slicing->plan_path, plan);
+        if (!e.empty()) return fail(ctx, TN_EINVAL, e);
+    } else {
+        e = tnb::find_plan(ctx->net, ctx->leaves, ctx->req, opt, plan);
+        if (!e.empty()) return fail(ctx, TN_EINFEASIBLE, e);
+    }
     if (slicing && slicing->companions) {
         // the companion edges change the network (exact basis changes) and the leaves: plan on a copy
         tnb::Network net2 = ctx->net;
@@ -182,19 +195,32 @@ tn_status tn_plan(tn_ctx* ctx, const tn_slicing* slicing, int64_t max_tensor_siz
     ctx->plan = plan;
     ctx->planned = true;
     ctx->sliced_wires.clear();
-    for (int eid : plan.sliced) {
-        ctx->sliced_wires.push_back(ctx->net.edges[eid].q);
-        ctx->sliced_wires.push_back(ctx->net.edges[eid].k);
+    ctx->local_wires.clear();
+    const int s_all = (int)plan.sliced.size();
+    const int s_glob = plan.segs.empty() ? s_all : plan.n_global;
+    for (int i = 0; i < s_all; i++) {
+        const int eid = plan.sliced[i];
+        auto& v = i < s_glob ? ctx->sliced_wires : ctx->local_wires;
+        v.push_back(ctx->net.edges[eid].q);
+        v.push_back(ctx->net.edges[eid].k);
     }
     tn_plan_info& I = ctx->info;
     I = tn_plan_info{};
-    I.s = (int32_t)plan.sliced.size();
+    I.s = (int32_t)s_glob;
+    I.s_local = (int32_t)(s_all - s_glob);
+    I.local_wires = ctx->local_wires.data();
+    I.n_segments = plan.segs.empty() ? 1 : (int32_t)plan.segs.size();
+    I.total_cmac = plan.segs.empty() ? std::ldexp(ctx->prog.cmac, s_all) + ctx->prog.pre_cmac : ctx->prog.total_cmac;
+    I.persist_bytes = ctx->prog.lvl_bytes;
     I.sliced_wires = ctx->sliced_wires.data();
     I.n_tensors = (int64_t)ctx->leaves.size();
     I.n_steps = ctx->prog.n_pairs;
     I.n_launches = (int64_t)ctx->prog.steps.size();
+    for (const auto& sg : ctx->prog.segs) I.n_launches += (int64_t)sg.steps.size();
     I.peak_elems = std::max<int64_t>(ctx->prog.peak_elems, 1);
-    I.workspace_bytes = ctx->prog.work_bytes;
+    // per pipeline: step workspace + the loop program's kept region (executor.cu dev_bind)
+    I.workspace_bytes = ((ctx->prog.work_bytes + 4095) & ~(int64_t)4095) +
+                        (ctx->prog.segs.empty() ? 0 : ((ctx->prog.lvl_bytes + 4095) & ~(int64_t)4095));
     I.cmac_per_slice = ctx->prog.cmac;
     I.bytes_per_slice = ctx->prog.bytes;
     I.gemm_cmac_per_slice = ctx->prog.gemm_cmac;
@@ -225,6 +251,14 @@ tn_status tn_plan_dump(const tn_ctx* ctx, const char* path) {
     return TN_OK;
 }
 
+tn_status tn_plan_save(const tn_ctx* ctx, const char* path) {
+    if (!ctx || !path) return TN_EINVAL;
+    if (!ctx->planned) return TN_EINVAL;
+    std::string e = tnb::save_plan(ctx->net, ctx->leaves, ctx->plan, path);
+    if (!e.empty()) return TN_EINVAL;
+    return TN_OK;
+}
+
 tn_status tn_bind_device(tn_ctx* ctx, int device, void* workspace, size_t bytes, void* cuda_stream) {
     if (!ctx) return TN_EINVAL;
     if (!ctx->planned) return fail(ctx, TN_EINVAL, "tn_bind_device before tn_plan");
@@ -247,7 +281,7 @@ tn_status tn_contract(tn_ctx* ctx, const uint64_t* slice_ids, int64_t n_ids, voi
     if (!ctx->dev) return fail(ctx, TN_EINVAL, "tn_contract before tn_bind_device");
     if (!slice_ids || n_ids < 1) return fail(ctx, TN_EINVAL, "empty slice subset");
     if (!amps_out) return fail(ctx, TN_EINVAL, "null amps_out");
-    const int s = (int)ctx->plan.sliced.size();
+    const int s = ctx->plan.segs.empty() ? (int)ctx->plan.sliced.size() : ctx->plan.n_global;
     std::vector<uint64_t> ids(slice_ids, slice_ids + n_ids);
     std::sort(ids.begin(), ids.end());
     for (int64_t i = 0; i < n_ids; i++) {

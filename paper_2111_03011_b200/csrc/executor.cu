@@ -114,6 +114,11 @@ struct Launch {
     std::vector<MemAcc> mem;     // workspace / persistent ranges read and written (graph dependencies)
     int a_region = REG_NONE, b_region = REG_NONE;  // apply operands' regions (tiny-step chains' preloads)
     int64_t a_off = 0, b_off = 0;
+    // K_ACCUM (loop-program summation)
+    const float2* c_src = nullptr;
+    float2* c_dst = nullptr;
+    int64_t c_n = 0;
+    uint64_t c_E = 0;
     // K_MULTI: a k_chain run of tiny steps
     size_t m_first = 0;          // index into Device::msteps_host
     int m_n = 0;
@@ -138,6 +143,14 @@ struct Pipe {
     std::vector<Launch> launches;
     std::vector<kern::MStep> msteps_host;
     kern::MStep* msteps = nullptr;
+    // loop program (Program::segs): one child per segment sharing this pipe's stream, workspace and
+    // accumulators; the loop index tau lives in device memory (written by k_set_tau before a segment runs)
+    char* lvl = nullptr;             // REG_LVL base (checkpoint stems, local-slice accumulators)
+    uint64_t* tau = nullptr;
+    int64_t* zero = nullptr;         // k_instantiate reads tau[*zero]
+    int64_t* rcounter = nullptr;     // k_readout's counter (unused in loop programs)
+    bool child = false;              // shares buffers with its parent (freed there)
+    std::vector<Pipe> seg;
 };
 
 struct Device {
@@ -156,10 +169,16 @@ struct Device {
     std::vector<Pipe> pipes;
     int64_t M = 0;
     int s = 0;
+    int s_global = 0;                // loop program: slice-id bits (tau = sigma << (s - s_global) | local)
+    struct SegMask {
+        uint64_t D, Sum, E;
+    };
+    std::vector<SegMask> segm;       // empty: flat program (one graph per slice)
     std::vector<cudaStream_t> capture_streams;  // fork streams used while capturing the graphs (DAG)
 };
 
 constexpr int kCaptureStreams = 4;  // + the pipeline's own stream
+constexpr int64_t kSliceCap = 4096;  // slice ids per upload (tn_contract feeds longer blocks in chunks)
 
 namespace {
 
@@ -254,9 +273,11 @@ void launch_apply_ni(const Launch& L, cudaStream_t st) {
     }
 }
 
-int set_smem_attrs(std::string& err) {
-    static bool done = false;
-    if (done) return TN_OK;
+int set_smem_attrs(int device, std::string& err) {
+    // cudaFuncSetAttribute applies to the current device: remember it per device
+    static uint64_t done_mask = 0;
+    const uint64_t bit = 1ull << (device & 63);
+    if (done_mask & bit) return TN_OK;
     const int big = 160 * 1024;
 #define SETA(NI, T) CK(cudaFuncSetAttribute(kern::k_apply<NI, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, big))
     SETA(0, 1); SETA(1, 1); SETA(2, 1); SETA(3, 1); SETA(4, 1);
@@ -280,7 +301,7 @@ int set_smem_attrs(std::string& err) {
                             tc::Cfg<128, 2>::SMEM));
     CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             tc::Cfg<256, 2>::SMEM));
-    done = true;
+    done_mask |= bit;
     return TN_OK;
 }
 
@@ -391,7 +412,10 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
             launch_gemm(L, st);
             break;
         case K_READOUT:
-            kern::k_readout<<<L.grid, L.block, 0, st>>>(L.F, L.ridx, P.acc, L.M, P.counter);
+            kern::k_readout<<<L.grid, L.block, 0, st>>>(L.F, L.ridx, P.acc, L.M, P.rcounter ? P.rcounter : P.counter);
+            break;
+        case K_ACCUM:
+            kern::k_accum<<<L.grid, L.block, 0, st>>>(L.c_src, L.c_dst, L.c_n, P.tau, L.c_E);
             break;
         case K_MULTI:
             kern::k_chain<<<1, 256, L.smem, st>>>(P.msteps + L.m_first, L.m_n);
@@ -682,6 +706,7 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
             case REG_BANK: return d->bank + b.offset;
             case REG_MAPS: return d->maps + b.offset;
             case REG_PERS: return d->pers + b.offset;
+            case REG_LVL: return P.lvl + b.offset;
             default: return nullptr;
         }
     };
@@ -1059,6 +1084,12 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
             L.ridx = (const int64_t*)ptr(st.rp.idx);
             L.M = st.rp.M;
             L.grid = grid_for(st.rp.M, 256, 148 * 8);
+        } else if (st.kind == K_ACCUM) {
+            L.c_src = (const float2*)ptr(st.cp.src);
+            L.c_dst = (float2*)ptr(st.cp.dst);
+            L.c_n = st.cp.n;
+            L.c_E = st.cp.E;
+            L.grid = grid_for((st.cp.n + 1) / 2, 256, 148 * 8);
         }
         P.launches.push_back(L);
     }
@@ -1086,18 +1117,25 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
         CK(cudaMemcpy(P.msteps, P.msteps_host.data(), P.msteps_host.size() * sizeof(kern::MStep),
                       cudaMemcpyHostToDevice));
     }
-    CK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&P.done, cudaEventDisableTiming));
-    CK(cudaMalloc(&P.acc, std::max<int64_t>(d->M, 1) * sizeof(double2)));
-    CK(cudaMalloc(&P.counter, sizeof(int64_t)));
-    P.slice_cap = 1024;
-    CK(cudaMalloc(&P.slice_ids, P.slice_cap * sizeof(uint64_t)));
-    CK(cudaMemset(P.slice_ids, 0, P.slice_cap * sizeof(uint64_t)));
-    CK(cudaMemset(P.counter, 0, sizeof(int64_t)));
-    // diagnostics only (tools/skip_exp.py): TNB_SKIP="k2,s56,x4_102" leaves launches of kind 2, of step 56 and
-    // the kind-4 launch of step 102 out of the captured graph, to measure each launch's marginal throughput
-    // cost under concurrent pipelines.  The amplitudes are then wrong; never set it otherwise.
+    if (!P.child) {
+        CK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&P.done, cudaEventDisableTiming));
+        CK(cudaMalloc(&P.acc, std::max<int64_t>(d->M, 1) * sizeof(double2)));
+        CK(cudaMalloc(&P.counter, sizeof(int64_t)));
+        // fixed capacity: the captured graph holds this pointer, so tn_contract feeds longer blocks in chunks
+        P.slice_cap = kSliceCap;
+        CK(cudaMalloc(&P.slice_ids, P.slice_cap * sizeof(uint64_t)));
+        CK(cudaMemset(P.slice_ids, 0, P.slice_cap * sizeof(uint64_t)));
+        CK(cudaMemset(P.counter, 0, sizeof(int64_t)));
+    }
+#ifdef TNB_DIAG_SKIP
+    // diagnostics builds only (-DTNB_DIAG_SKIP, tools/skip_exp.py): TNB_SKIP="k2,s56,x4_102" leaves launches of
+    // kind 2, of step 56 and the kind-4 launch of step 102 out of the captured graph, to measure each launch's
+    // marginal throughput cost under concurrent pipelines.  The amplitudes are then wrong.
     std::string skip = getenv("TNB_SKIP") ? std::string(",") + getenv("TNB_SKIP") + "," : std::string();
+#else
+    const std::string skip;
+#endif
     std::vector<int> keep;
     for (int i = 0; i < (int)P.launches.size(); i++) {
         const Launch& L = P.launches[i];
@@ -1213,7 +1251,7 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
         return TN_ECUDA;
     }
     {
-        int rc = set_smem_attrs(err);
+        int rc = set_smem_attrs(device, err);
         if (rc) return fail(rc);
     }
     d->user = (cudaStream_t)stream;
@@ -1228,12 +1266,15 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
     CKF(cudaEventCreate(&d->ev0));
     CKF(cudaEventCreate(&d->ev1));
     CKF(cudaEventCreateWithFlags(&d->evu, cudaEventDisableTiming));
-    const int64_t wb = (prog.work_bytes + 4095) & ~(int64_t)4095;
+    // per pipeline: the step workspace followed by the loop program's kept region (REG_LVL)
+    const int64_t wb0 = (prog.work_bytes + 4095) & ~(int64_t)4095;
+    const int64_t lb = prog.segs.empty() ? 0 : ((prog.lvl_bytes + 4095) & ~(int64_t)4095);
+    const int64_t wb = wb0 + lb;
     int np = 1;
     if (workspace) {
-        if ((int64_t)bytes < prog.work_bytes) {
+        if ((int64_t)bytes < wb) {
             std::ostringstream o;
-            o << "workspace too small: need " << prog.work_bytes << " bytes, got " << bytes;
+            o << "workspace too small: need " << wb << " bytes, got " << bytes;
             err = o.str();
             return fail(TN_ENOMEM);
         }
@@ -1261,11 +1302,45 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
         int rc = build_pipe(d, d->pre, prog.pre_steps, err);
         if (rc) return fail(rc);
     }
+    d->s_global = prog.segs.empty() ? prog.s : prog.s_global;
+    for (const auto& g : prog.segs) d->segm.push_back({g.D, g.Sum, g.E});
     d->pipes.resize(np);
     for (int p = 0; p < np; p++) {
-        d->pipes[p].work = d->work_all + (size_t)p * wb;
-        int rc = build_pipe(d, d->pipes[p], prog.steps, err);
-        if (rc) return fail(rc);
+        Pipe& P = d->pipes[p];
+        P.work = d->work_all + (size_t)p * wb;
+        P.lvl = P.work + wb0;
+        if (prog.segs.empty()) {
+            int rc = build_pipe(d, P, prog.steps, err);
+            if (rc) return fail(rc);
+            continue;
+        }
+        // loop program: the parent owns stream, accumulator and tau; one child graph per segment
+        CKF(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+        CKF(cudaEventCreateWithFlags(&P.done, cudaEventDisableTiming));
+        CKF(cudaMalloc(&P.acc, std::max<int64_t>(M, 1) * sizeof(double2)));
+        CKF(cudaMalloc(&P.counter, sizeof(int64_t)));
+        CKF(cudaMalloc(&P.tau, sizeof(uint64_t)));
+        CKF(cudaMalloc(&P.zero, sizeof(int64_t)));
+        CKF(cudaMalloc(&P.rcounter, sizeof(int64_t)));
+        CKF(cudaMemset(P.counter, 0, sizeof(int64_t)));
+        CKF(cudaMemset(P.tau, 0, sizeof(uint64_t)));
+        CKF(cudaMemset(P.zero, 0, sizeof(int64_t)));
+        CKF(cudaMemset(P.rcounter, 0, sizeof(int64_t)));
+        P.seg.resize(prog.segs.size());
+        for (size_t j = 0; j < prog.segs.size(); j++) {
+            Pipe& C = P.seg[j];
+            C.child = true;
+            C.stream = P.stream;
+            C.work = P.work;
+            C.lvl = P.lvl;
+            C.acc = P.acc;
+            C.tau = P.tau;
+            C.slice_ids = P.tau;
+            C.counter = P.zero;
+            C.rcounter = P.rcounter;
+            int rc = build_pipe(d, C, prog.segs[j].steps, err);
+            if (rc) return fail(rc);
+        }
     }
 #undef CKF
     *out = d;
@@ -1292,26 +1367,80 @@ int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_ou
         CK(cudaEventRecord(d->evu, d->pre.stream));
     }
     std::vector<double2*> accs;
-    for (int p = 0; p < (int)d->pipes.size(); p++) {
-        Pipe& P = d->pipes[p];
+    std::vector<int64_t> pstart(np), pcnt(np);
+    for (int p = 0; p < np; p++) {
         // contiguous block p of the ascending slice list (sizes differ by <= 1)
         const int64_t base = n / np, extra = n % np;
-        const int64_t start = (p < np) ? p * base + std::min<int64_t>(p, extra) : n;
-        const int64_t cnt = (p < np) ? base + (p < extra ? 1 : 0) : 0;
-        if (cnt == 0) continue;
-        if (cnt > P.slice_cap) {
-            CK(cudaFree(P.slice_ids));
-            P.slice_cap = std::max<int64_t>(cnt, 2 * P.slice_cap);
-            CK(cudaMalloc(&P.slice_ids, P.slice_cap * sizeof(uint64_t)));
-        }
+        pstart[p] = p * base + std::min<int64_t>(p, extra);
+        pcnt[p] = base + (p < extra ? 1 : 0);
+    }
+    for (int p = 0; p < np; p++) {
+        Pipe& P = d->pipes[p];
+        if (pcnt[p] == 0) continue;
         CK(cudaStreamWaitEvent(P.stream, d->evu, 0));
-        CK(cudaMemcpyAsync(P.slice_ids, ids_sorted + start, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice, P.stream));
         CK(cudaMemsetAsync(P.acc, 0, d->M * sizeof(double2), P.stream));
-        CK(cudaMemsetAsync(P.counter, 0, sizeof(int64_t), P.stream));
-        for (int64_t i = 0; i < cnt; i++) CK(cudaGraphLaunch(P.gexec, P.stream));
-        CK(cudaEventRecord(P.done, P.stream));
         accs.push_back(P.acc);
     }
+    if (d->segm.empty()) {
+        // flat program: the slice graph reads slice_ids[*counter] (incremented by the readout); blocks longer
+        // than the id buffer are fed in chunks (the graph holds the buffer's address)
+        for (int p = 0; p < np; p++) {
+            Pipe& P = d->pipes[p];
+            for (int64_t c0 = 0; c0 < pcnt[p]; c0 += P.slice_cap) {
+                const int64_t c = std::min<int64_t>(P.slice_cap, pcnt[p] - c0);
+                CK(cudaMemcpyAsync(P.slice_ids, ids_sorted + pstart[p] + c0, c * sizeof(uint64_t),
+                                   cudaMemcpyHostToDevice, P.stream));
+                CK(cudaMemsetAsync(P.counter, 0, sizeof(int64_t), P.stream));
+                for (int64_t i = 0; i < c; i++) CK(cudaGraphLaunch(P.gexec, P.stream));
+            }
+        }
+    } else {
+        // loop program: tau = sigma << l | local runs through the local values of every slice in order; a
+        // segment runs when all its Sum bits are 1 (the summations it reads are complete) and its D bits
+        // differ from its previous run (otherwise its kept outputs are still valid: head reuse)
+        const int l = d->s - d->s_global;
+        const int J = (int)d->segm.size();
+        struct It {
+            int64_t i = 0;
+            std::vector<uint64_t> last;
+            std::vector<char> ran;
+        };
+        std::vector<It> its(np);
+        for (int p = 0; p < np; p++) {
+            its[p].last.assign(J, 0);
+            its[p].ran.assign(J, 0);
+        }
+        bool more = true;
+        while (more) {  // round-robin over pipelines, one slice at a time
+            more = false;
+            for (int p = 0; p < np; p++) {
+                if (its[p].i >= pcnt[p]) continue;
+                Pipe& P = d->pipes[p];
+                const uint64_t sigma = ids_sorted[pstart[p] + its[p].i];
+                for (uint64_t loc = 0; loc < (1ull << l); loc++) {
+                    const uint64_t tau = (sigma << l) | loc;
+                    bool set = false;
+                    for (int j = 0; j < J; j++) {
+                        const Device::SegMask& g = d->segm[j];
+                        if ((tau & g.Sum) != g.Sum) continue;
+                        const uint64_t dv = tau & g.D;
+                        if (its[p].ran[j] && its[p].last[j] == dv) continue;
+                        if (!set) {
+                            kern::k_set_tau<<<1, 1, 0, P.stream>>>(P.tau, tau);
+                            set = true;
+                        }
+                        CK(cudaGraphLaunch(P.seg[j].gexec, P.stream));
+                        its[p].ran[j] = 1;
+                        its[p].last[j] = dv;
+                    }
+                }
+                its[p].i++;
+                more = more || its[p].i < pcnt[p];
+            }
+        }
+    }
+    for (int p = 0; p < np; p++)
+        if (pcnt[p]) CK(cudaEventRecord(d->pipes[p].done, d->pipes[p].stream));
     if (trace) tA = now_ms();
     Pipe& P0 = d->pipes[0];
     for (int p = 1; p < np; p++) CK(cudaStreamWaitEvent(P0.stream, d->pipes[p].done, 0));
@@ -1359,15 +1488,25 @@ int dev_profile(Device* d, uint64_t slice_id, tn_launch_stat* stats, int max_sta
         CK(cudaStreamSynchronize(d->pre.stream));
     }
     Pipe& P = d->pipes[0];
-    CK(cudaMemcpyAsync(P.slice_ids, &slice_id, sizeof(uint64_t), cudaMemcpyHostToDevice, P.stream));
+    // loop program: one pass through every segment at tau = slice_id << l (timing only)
+    std::vector<std::pair<Pipe*, const Launch*>> seq;
+    if (d->segm.empty()) {
+        CK(cudaMemcpyAsync(P.slice_ids, &slice_id, sizeof(uint64_t), cudaMemcpyHostToDevice, P.stream));
+        for (const Launch& L : P.launches) seq.push_back({&P, &L});
+    } else {
+        const uint64_t tau = slice_id << (d->s - d->s_global);
+        kern::k_set_tau<<<1, 1, 0, P.stream>>>(P.tau, tau);
+        for (Pipe& C : P.seg)
+            for (const Launch& L : C.launches) seq.push_back({&C, &L});
+    }
     CK(cudaMemsetAsync(P.counter, 0, sizeof(int64_t), P.stream));
     CK(cudaMemsetAsync(P.acc, 0, d->M * sizeof(double2), P.stream));
-    const int nl = (int)P.launches.size();
+    const int nl = (int)seq.size();
     std::vector<cudaEvent_t> ev(nl + 1);
     for (auto& e : ev) CK(cudaEventCreate(&e));
     CK(cudaEventRecord(ev[0], P.stream));
     for (int i = 0; i < nl; i++) {
-        do_launch(d, P, P.launches[i], P.stream);
+        do_launch(d, *seq[i].first, *seq[i].second, P.stream);
         CK(cudaGetLastError());
         CK(cudaEventRecord(ev[i + 1], P.stream));
     }
@@ -1376,7 +1515,7 @@ int dev_profile(Device* d, uint64_t slice_id, tn_launch_stat* stats, int max_sta
     for (int i = 0; i < nl && w < max_stats; i++, w++) {
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
-        const Launch& L = P.launches[i];
+        const Launch& L = *seq[i].second;
         tn_launch_stat& s = stats[w];
         s.kind = L.kind;
         s.step = L.pair;
@@ -1397,6 +1536,8 @@ int dev_pipes(const Device* d) { return d ? (int)d->pipes.size() : 0; }
 
 void dev_launch_counts(const Device* d, int64_t* per_slice, int64_t* per_contract) {
     *per_slice = d->pipes.empty() ? 0 : (int64_t)d->pipes[0].launches.size();
+    if (!d->pipes.empty())  // loop program: one pass through every segment
+        for (const Pipe& C : d->pipes[0].seg) *per_slice += (int64_t)C.launches.size();
     *per_contract = (d->has_pre ? (int64_t)d->pre.launches.size() : 0) + 1;  // + k_finalize / k_sum_pipes
 }
 
@@ -1406,6 +1547,15 @@ void dev_destroy(Device* d) {
     if (d->has_pre) d->pipes.push_back(d->pre);  // freed with the others below
     for (Pipe& P : d->pipes) {
         if (P.stream) cudaStreamSynchronize(P.stream);
+        for (Pipe& C : P.seg) {
+            if (C.gexec) cudaGraphExecDestroy(C.gexec);
+            if (C.graph) cudaGraphDestroy(C.graph);
+            cudaFree(C.tables);
+            cudaFree(C.msteps);
+        }
+        cudaFree(P.tau);
+        cudaFree(P.zero);
+        cudaFree(P.rcounter);
         if (P.gexec) cudaGraphExecDestroy(P.gexec);
         if (P.graph) cudaGraphDestroy(P.graph);
         cudaFree(P.tables);
@@ -1434,7 +1584,11 @@ void dev_destroy(Device* d) {
 // (prep A / prep B / tcgen05 GEMM).  M % 128 may be ragged; N >= 64 and K >= 16 powers of two.
 int debug_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K, int ea, void* stream,
                std::string& err) {
-    if (set_smem_attrs(err)) return TN_ECUDA;
+    {
+        int dv = 0;
+        cudaGetDevice(&dv);
+        if (set_smem_attrs(dv, err)) return TN_ECUDA;
+    }
     if (N < 16 || K < 16 || (N & (N - 1)) || (K & (K - 1))) {
         err = "debug_gemm: N >= 16 and K >= 16 must be powers of two";
         return TN_EINVAL;

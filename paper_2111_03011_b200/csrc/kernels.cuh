@@ -73,8 +73,9 @@ constexpr int ROWS_SMEM_MAX = 112 * 1024;  // k_apply_rows: tables + both parent
 #ifndef TNB_APPLY_MINB
 #define TNB_APPLY_MINB 3  // 3 CTAs per SM (<= 80 registers): measured 2544 vs 2385 slices/s with 2
 #endif
+// the 16-output warp-team variant needs more than 80 registers (it spilled 108 B at 3 CTAs/SM): 2 CTAs/SM
 template <int NI, int TEAM>
-__global__ void __launch_bounds__(256, TNB_APPLY_MINB) k_apply(const ApplyDev p) {
+__global__ void __launch_bounds__(256, (NI == 4 && TEAM == 32) ? 2 : TNB_APPLY_MINB) k_apply(const ApplyDev p) {
     extern __shared__ uint32_t sm[];
     const int tabn = p.ntab * 256 * 4;
     for (int i = threadIdx.x; i < tabn; i += blockDim.x) sm[i] = p.tab[i];
@@ -714,6 +715,37 @@ __global__ void k_readout(const float2* __restrict__ F, const int64_t* __restric
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *counter += 1;
 }
+
+// Loop program (local slices): dst = src on the first value of the summed bits E of tau, else
+// dst + src.  Elementwise over n complex64 values (float4 = two complex values per thread step).
+__global__ void k_accum(const float2* __restrict__ src, float2* __restrict__ dst, int64_t n,
+                        const uint64_t* __restrict__ tau, uint64_t E) {
+    const bool first = (*tau & E) == 0;
+    const int64_t n2 = n >> 1;
+    const float4* s4 = (const float4*)src;
+    float4* d4 = (float4*)dst;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 v = s4[i];
+        if (!first) {
+            const float4 a = d4[i];
+            v.x += a.x;
+            v.y += a.y;
+            v.z += a.z;
+            v.w += a.w;
+        }
+        d4[i] = v;
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        float2 v = src[n - 1];
+        if (!first) {
+            v.x += dst[n - 1].x;
+            v.y += dst[n - 1].y;
+        }
+        dst[n - 1] = v;
+    }
+}
+
+__global__ void k_set_tau(uint64_t* __restrict__ tau, uint64_t v) { *tau = v; }
 
 __global__ void k_finalize(const double2* __restrict__ acc, float2* __restrict__ out, int64_t M) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x)

@@ -98,6 +98,36 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     for (const auto& t : plan.tied) slice_index[t.first] = t.second;  // companion edges share the bit
     Alloc wa;  // per-slice workspace (reused between steps)
     Alloc pa;  // persistent region for slice-invariant results (read by every slice)
+    Alloc la;  // loop program: tensors kept across loop iterations (checkpoint stems, accumulators)
+    const bool segmented = !plan.segs.empty();
+    const int n_seg = segmented ? (int)plan.segs.size() : 0;
+    if (segmented) {
+        if (plan.step_seg.size() != plan.order.size()) return "loop program: step_seg length differs from the order";
+        if (plan.n_global < 0 || plan.n_global > s) return "loop program: bad n_global";
+        prog.segs.resize(n_seg);
+        for (int j = 0; j < n_seg; j++) {
+            prog.segs[j].D = plan.segs[j].D;
+            prog.segs[j].Sum = plan.segs[j].Sum;
+            prog.segs[j].E = plan.segs[j].E;
+            if (plan.segs[j].E & ~plan.segs[j].D) return "loop program: a segment sums a bit it does not loop over";
+        }
+        const uint64_t local = (s - plan.n_global) >= 64 ? ~0ull : ((1ull << (s - plan.n_global)) - 1);
+        if (plan.segs.back().E != 0) return "loop program: the last segment cannot sum local bits";
+        if (plan.segs.back().Sum != local) return "loop program: the last segment must follow every local summation";
+        prog.s_global = plan.n_global;
+    } else {
+        prog.s_global = s;
+    }
+    // tau-bit mask of every sliced edge (natural dependencies, checked against the segments)
+    auto tau_bit = [&](int e) -> uint64_t {
+        auto it = slice_index.find(e);
+        return it == slice_index.end() ? 0ull : (1ull << (s - 1 - it->second));
+    };
+    std::vector<uint64_t> nat(leaves.size(), 0);
+    std::vector<InstLeafDesc> leaf_desc(leaves.size());
+    std::vector<char> leaf_pending(leaves.size(), 0);     // segmented: instantiated when first consumed
+    std::vector<std::vector<InstLeafDesc>> seg_inst(n_seg);
+    std::vector<int64_t> seg_items(n_seg, 0);
     std::vector<LT> slot(leaves.size());
     std::ostringstream js;
     js.precision(17);
@@ -106,7 +136,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     js << "],\"leaves\":[";
 
     auto acc = [](Step& st, const BufRef& b, int64_t bytes, bool write) {
-        if (b.region != REG_WORK && b.region != REG_PERS) return;
+        if (b.region != REG_WORK && b.region != REG_PERS && b.region != REG_LVL) return;
         MemAcc m;
         m.region = b.region;
         m.write = write ? 1 : 0;
@@ -151,12 +181,19 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             for (int j = 0; j < d.n_sl; j++) {
                 d.sl_pos[j] = (int8_t)bitpos(L.legs, sl[j]);
                 d.sl_idx[j] = (int8_t)slice_index[sl[j]];
+                nat[li] |= tau_bit(sl[j]);
             }
             t.bytes = d.items * 8;
-            int64_t off = wa.alloc(t.bytes);
-            d.out_off = off;
-            t.buf = BufRef{REG_WORK, off};
-            inst.push_back(d);
+            if (segmented) {
+                inst_items -= d.items;
+                leaf_desc[li] = d;
+                leaf_pending[li] = 1;
+            } else {
+                int64_t off = wa.alloc(t.bytes);
+                d.out_off = off;
+                t.buf = BufRef{REG_WORK, off};
+                inst.push_back(d);
+            }
         }
         js << (li ? "," : "") << "{\"tensor\":" << L.tensor_id << ",\"qmask\":" << L.qmask << ",\"rows\":" << L.rows.size()
            << ",\"legs\":[";
@@ -177,9 +214,44 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
 
     // ---------------------------------------------------------------- pairwise steps
     int final_slot = plan.order.empty() ? 0 : plan.order.back().first;
+    // consumer step of each step's result (segmented: results consumed in another segment persist)
+    std::vector<int> consumer(plan.order.size(), -1);
+    {
+        std::vector<int> last_writer(leaves.size(), -1);
+        for (size_t p = 0; p < plan.order.size(); p++) {
+            const int i = plan.order[p].first, j = plan.order[p].second;
+            if (last_writer[i] >= 0) consumer[last_writer[i]] = (int)p;
+            if (last_writer[j] >= 0) consumer[last_writer[j]] = (int)p;
+            last_writer[i] = (int)p;
+        }
+    }
+    // segmented: the segment that first consumes each sliced leaf instantiates it (in every run)
+    std::vector<int> leaf_seg(leaves.size(), -1);
+    if (segmented)
+        for (size_t p = 0; p < plan.order.size(); p++)
+            for (int li : {plan.order[p].first, plan.order[p].second})
+                if (leaf_pending[li] && leaf_seg[li] < 0) leaf_seg[li] = plan.step_seg[p];
     for (size_t p = 0; p < plan.order.size(); p++) {
         int i = plan.order[p].first, j = plan.order[p].second;
+        const int sg = segmented ? plan.step_seg[p] : -1;
+        if (segmented && (p == 0 || plan.step_seg[p - 1] != sg)) {
+            // K_INSTANTIATE runs first in the segment: all of its leaves get their buffers now, before any
+            // step of the segment allocates a temporary (no overlap with the segment's other tensors)
+            for (size_t li = 0; li < leaves.size(); li++) {
+                if (!leaf_pending[li] || leaf_seg[li] != sg) continue;
+                InstLeafDesc d = leaf_desc[li];
+                d.item_begin = seg_items[sg];
+                seg_items[sg] += d.items;
+                d.out_off = wa.alloc(slot[li].bytes);
+                slot[li].buf = BufRef{REG_WORK, d.out_off};
+                seg_inst[sg].push_back(d);
+                leaf_pending[li] = 0;
+            }
+        }
         LT X = slot[i], Y = slot[j];
+        const uint64_t natC = nat[i] | nat[j];
+        if (segmented && (natC & ~plan.segs[sg].D))
+            return "loop program: step " + std::to_string(p) + " depends on a sliced bit its segment does not loop over";
         std::vector<int> K;
         for (int e : X.legs)
             if (has(Y.legs, e)) K.push_back(e);
@@ -237,9 +309,19 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         // (the sliced-network analogue of the paper's head-result reuse)
         const bool var = X.variant || Y.variant;
         std::string apply_json, gemm_json;
-        Alloc& al = var ? wa : pa;
-        const int32_t reg = var ? REG_WORK : REG_PERS;
-        std::vector<Step>& out = var ? prog.steps : prog.pre_steps;
+        // segmented: a variant result consumed by another segment is kept across loop iterations
+        // (REG_LVL), unless the segment ends with a summation (then the accumulator is the kept copy)
+        const bool seg_last = segmented && (p + 1 == plan.order.size() || plan.step_seg[p + 1] != sg);
+        const bool accum = segmented && var && seg_last && plan.segs[sg].E != 0;
+        const bool keep = segmented && var && !accum && consumer[p] >= 0 && plan.step_seg[consumer[p]] != sg;
+        Alloc& al0 = var ? wa : pa;
+        const int32_t reg0 = var ? REG_WORK : REG_PERS;
+        std::vector<Step>& out = var ? (segmented ? prog.segs[sg].steps : prog.steps) : prog.pre_steps;
+        // the result's allocator; operands' temporaries (prep buffers) always come from al0
+        Alloc& alC = keep ? la : al0;
+        const int32_t regC = keep ? REG_LVL : reg0;
+        Alloc& al = al0;
+        const int32_t reg = reg0;
         LT Cn;
         Cn.qmask = qC;
         Cn.rows = rowsC;
@@ -299,8 +381,8 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             ap.n_inner = (int)std::min<size_t>(4, fbpos.size());
             for (int t = 0; t < ap.n_inner; t++) ap.inner_c[t] = (int8_t)fbpos[t];
             Cn.bytes = RC * ap.c_row * 8;
-            int64_t off = al.alloc(Cn.bytes);
-            Cn.buf = BufRef{reg, off};
+            int64_t off = alC.alloc(Cn.bytes);
+            Cn.buf = BufRef{regC, off};
             ap.C = Cn.buf;
             ap.a_elems = sizeA;
             ap.b_elems = sizeB;
@@ -440,7 +522,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             gp.Bhi = BufRef{reg, al.alloc(bbytes)};
             gp.Blo = BufRef{reg, al.alloc(bbytes)};
             Cn.bytes = RC * m * n * 8;
-            Cn.buf = BufRef{reg, al.alloc(Cn.bytes)};
+            Cn.buf = BufRef{regC, alC.alloc(Cn.bytes)};
             gp.C = Cn.buf;
             Step sa;
             sa.kind = K_PREP_A;
@@ -480,8 +562,34 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         }
         if (var) prog.cmac += cmac;
         else prog.pre_cmac += cmac;
+        if (segmented && var) prog.total_cmac += cmac * std::ldexp(1.0, __builtin_popcountll(plan.segs[sg].D));
+        nat[i] = natC;
+        if (accum) {
+            // local-slice summation: acc = (first value of the E bits ? 0 : acc) + C, kept across iterations
+            if ((natC & plan.segs[sg].E) != plan.segs[sg].E)
+                return "loop program: segment " + std::to_string(sg) + " sums bits its last step does not depend on";
+            const int64_t n_el = RC << Cn.legs.size();
+            Step sa;
+            sa.kind = K_ACCUM;
+            sa.pair = (int)p;
+            sa.cp.src = Cn.buf;
+            sa.cp.n = n_el;
+            sa.cp.E = plan.segs[sg].E;
+            const BufRef accb{REG_LVL, la.alloc(n_el * 8)};
+            sa.cp.dst = accb;
+            sa.bytes = 24.0 * n_el;
+            acc(sa, Cn.buf, n_el * 8, false);
+            prog.segs[sg].steps.push_back(sa);
+            prog.total_cmac += 0.0;
+            wa.release(Cn.buf.offset, Cn.bytes);
+            Cn.buf = accb;
+            nat[i] = natC & ~plan.segs[sg].E;
+        } else if (segmented && var && keep && consumer[p] >= 0) {
+            // only the stem may carry the summed bits out of a segment
+            (void)0;
+        }
         prog.peak_elems = std::max<int64_t>(prog.peak_elems, RC << Cn.legs.size());
-        // release operands held in the workspace
+        // release operands held in the workspace (REG_LVL tensors stay for the whole loop program)
         if (X.buf.region == REG_WORK) wa.release(X.buf.offset, X.bytes);
         if (Y.buf.region == REG_WORK) wa.release(Y.buf.offset, Y.bytes);
         // persistent results consumed by another invariant step can be recycled inside the prologue;
@@ -530,7 +638,27 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     st.rp.idx = BufRef{REG_MAPS, push_blob(prog.maps, idx.data(), idx.size() * 8)};
     st.bytes = (8.0 + 8.0 + 32.0) * (double)req.M;
     acc(st, F.buf, ((int64_t)F.rows.size() << dF) * 8, false);
-    prog.steps.push_back(st);
+    if (segmented) {
+        const uint64_t glob = plan.n_global == 0 ? 0ull : (((1ull << plan.n_global) - 1) << (s - plan.n_global));
+        if (nat[final_slot] & ~glob) return "loop program: the final tensor still depends on a local bit";
+        prog.segs.back().steps.push_back(st);
+        // K_INSTANTIATE first in every segment that instantiates sliced leaves
+        for (int j = 0; j < n_seg; j++) {
+            if (seg_inst[j].empty()) continue;
+            Step si;
+            si.kind = K_INSTANTIATE;
+            si.ip.n_items = seg_items[j];
+            si.ip.n_leaves = (int32_t)seg_inst[j].size();
+            si.ip.table = BufRef{REG_MAPS, push_blob(prog.maps, seg_inst[j].data(), seg_inst[j].size() * sizeof(InstLeafDesc))};
+            si.bytes = 16.0 * seg_items[j];
+            for (const InstLeafDesc& d : seg_inst[j]) acc(si, BufRef{REG_WORK, d.out_off}, d.items * 8, true);
+            prog.segs[j].steps.insert(prog.segs[j].steps.begin(), si);
+        }
+        prog.lvl_bytes = la.peak;
+    } else {
+        prog.steps.push_back(st);
+        prog.lvl_bytes = 0;
+    }
 
     js << "],\"final\":{\"qmask\":" << F.qmask << ",\"rows\":" << F.rows.size() << ",\"legs\":[";
     for (int t = 0; t < dF; t++) js << (t ? "," : "") << wire_str(net, F.legs[t]);
@@ -546,6 +674,10 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     prog.work_bytes = std::max<int64_t>(wa.peak, 1024);
     prog.pers_bytes = std::max<int64_t>(pa.peak, 1024);
     for (const Step& x : prog.steps) prog.bytes += x.bytes;
+    for (const auto& sg : prog.segs)
+        for (const Step& x : sg.steps) prog.bytes += x.bytes;
+    if (!segmented) prog.total_cmac = std::ldexp(prog.cmac, s) + prog.pre_cmac;
+    else prog.total_cmac += prog.pre_cmac;
     // largest leaf counts toward the peak as well
     for (const LT& t : slot) (void)t;
     return "";

@@ -17,6 +17,8 @@
 #include <sstream>
 #include <functional>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <unordered_map>
 
@@ -28,20 +30,26 @@ namespace tnb {
 
 double RowModel::rows(uint64_t qmask) {
     if (qmask == 0) return 1.0;
-    for (auto& kv : memo)
-        if (kv.first == qmask) return kv.second;
+    auto it = memo.find(qmask);
+    if (it != memo.end()) return it->second;
     double r;
-    const double L = (double)req->fixed.size();
     if (req->fixed.size() <= (1u << 16)) {
         r = (double)rows_of(*req, qmask).size();
-    } else {  // expected distinct count of L uniform keys over 2^q values
-        const int q = __builtin_popcountll(qmask);
-        const double V = std::ldexp(1.0, q);
-        r = V * (1.0 - std::exp(L * std::log1p(-1.0 / V)));
-        r = std::max(1.0, std::min(r, L));
+    } else {
+        r = estimate(qmask);
     }
-    memo.push_back({qmask, r});
+    memo[qmask] = r;
     return r;
+}
+
+// expected number of distinct keys when L uniform fixed parts are projected onto 2^|q| values
+double RowModel::estimate(uint64_t qmask) const {
+    if (qmask == 0) return 1.0;
+    const double L = (double)req->fixed.size();
+    const int q = __builtin_popcountll(qmask);
+    const double V = std::ldexp(1.0, q);
+    double r = V * (1.0 - std::exp(L * std::log1p(-1.0 / V)));
+    return std::max(1.0, std::min(r, L));
 }
 
 namespace {
@@ -564,6 +572,400 @@ Tree rb_tree(const std::vector<Leaf>& leaves, const Graph& g, RowModel& rm, doub
     return t;
 }
 
+// ------------------------------------------------------------------------------ multilevel bisection trees
+// Recursive multilevel hypergraph bisection (partition.cpp).  Nets: one per internal bond (weight 1 = one
+// index bit), plus the "rows" net over the row-carrying leaves of the part (weight rows_w bits: splitting the
+// sparse output boundary across both halves makes both carry rows).  Parts of <= cutoff leaves are finished
+// greedily; subtree reconfiguration later re-optimises the small subtrees exactly.
+struct RB2 {
+    const std::vector<Leaf>* leaves;
+    const Network* net;
+    const std::vector<int>* slot_of_tensor;
+    const std::vector<int>* internal;
+    RowModel* rm;
+    double eps_lo, eps_hi;
+    int cutoff, rows_w;
+    double fix_ext;  // probability that a bisection pins the part's external legs to one side
+};
+
+int rb2_rec(Tree& t, const std::vector<int>& V, const RB2& P, std::mt19937_64& rng, int depth) {
+    if ((int)V.size() <= P.cutoff) return greedy_sub(t, V, *P.rm);
+    std::unordered_map<int, int> loc;
+    for (int i = 0; i < (int)V.size(); i++) loc[V[i]] = i;
+    HyperGraph g;
+    g.n = (int)V.size();
+    g.node_w.assign(g.n, 1);
+    for (int e : *P.internal) {
+        auto a = loc.find((*P.slot_of_tensor)[P.net->edges[e].t0]);
+        auto b = loc.find((*P.slot_of_tensor)[P.net->edges[e].t1]);
+        if (a == loc.end() || b == loc.end() || a->second == b->second) continue;
+        g.nets.push_back({a->second, b->second});
+        g.net_w.push_back(1);
+    }
+    if (P.rows_w > 0) {
+        std::vector<int> rp;
+        for (int i = 0; i < g.n; i++)
+            if ((*P.leaves)[V[i]].qmask) rp.push_back(i);
+        if (rp.size() >= 2) {
+            g.nets.push_back(rp);
+            g.net_w.push_back(P.rows_w);
+        }
+    }
+    // external legs (bonds to tensors outside V, open output legs): with probability fix_ext they are
+    // pinned to one side through a weightless fixed node, so that one half takes the part's boundary and
+    // the other is a compact branch with a small cut (stem-and-branch trees)
+    if (depth > 0 && (rng() % 1000) < P.fix_ext * 1000) {
+        const int X = g.n++;
+        g.node_w.push_back(0);
+        g.fixed.assign(g.n, -1);
+        g.fixed[X] = 0;
+        for (int i = 0; i < X; i++) {
+            int ext = 0;
+            for (int e : (*P.leaves)[V[i]].legs) {
+                const Edge& E = P.net->edges[e];
+                if (E.t1 < 0) { ext++; continue; }
+                const int o = (*P.slot_of_tensor)[E.t0] == V[i] ? E.t1 : E.t0;
+                if (!loc.count((*P.slot_of_tensor)[o])) ext++;
+            }
+            if (ext) {
+                g.nets.push_back({i, X});
+                g.net_w.push_back(ext);
+            }
+        }
+    }
+    // imbalance drawn per bisection from [eps_lo, eps_hi]
+    const double eps = P.eps_lo + (P.eps_hi - P.eps_lo) * ((rng() % 10000) / 10000.0);
+    std::vector<char> side = ml_bisect(g, eps, rng, 8);
+    static const int vb = getenv("TNB_PLAN_VERBOSE") ? atoi(getenv("TNB_PLAN_VERBOSE")) : 0;
+    if (vb >= 2 && depth <= 3) {
+        int64_t c = 0;
+        for (size_t e = 0; e < g.nets.size(); e++) {
+            bool s0 = false, s1 = false;
+            for (int v : g.nets[e]) (side[v] ? s1 : s0) = true;
+            if (s0 && s1) c += g.net_w[e];
+        }
+        int n0 = 0;
+        for (int i = 0; i < (int)V.size(); i++) n0 += !side[i];
+        fprintf(stderr, "%*s[rb2] depth %d |V| %zu eps %.2f -> %d / %zu cut %lld\n", 2 * depth, "", depth, V.size(), eps, n0,
+                V.size() - n0, (long long)c);
+    }
+    std::vector<int> A, B;
+    for (int i = 0; i < (int)V.size(); i++) (side[i] ? B : A).push_back(V[i]);
+    if (A.empty() || B.empty()) return greedy_sub(t, V, *P.rm);
+    int a = rb2_rec(t, A, P, rng, depth + 1);
+    int b = rb2_rec(t, B, P, rng, depth + 1);
+    Node N;
+    N.left = a;
+    N.right = b;
+    N.legs = t.nodes[a].legs ^ t.nodes[b].legs;
+    N.q = t.nodes[a].q | t.nodes[b].q;
+    N.rows = P.rm->rows(N.q);
+    int id = (int)t.nodes.size();
+    t.nodes[a].parent = id;
+    t.nodes[b].parent = id;
+    t.nodes.push_back(N);
+    return id;
+}
+
+Tree rb2_tree(const RB2& P, std::mt19937_64& rng) {
+    const std::vector<Leaf>& leaves = *P.leaves;
+    const int NL = (int)leaves.size();
+    Tree t;
+    t.nodes.resize(NL);
+    for (int i = 0; i < NL; i++) {
+        Node& N = t.nodes[i];
+        N.leaf = i;
+        for (int e : leaves[i].legs) N.legs.set(e);
+        N.q = leaves[i].qmask;
+        N.rows = (double)leaves[i].rows.size();
+    }
+    std::vector<int> V(NL);
+    for (int i = 0; i < NL; i++) V[i] = i;
+    t.root = rb2_rec(t, V, P, rng, 0);
+    return t;
+}
+
+// ------------------------------------------------------------------------------ sweep (stem) orders
+// A linear order pi of the leaves defines a stem tree: the stem absorbs pi[1], pi[2], ... one at a time
+// (P:L429's head and tail are stems absorbing branches).  Step k costs rows(Q_k) * 2^|dV_{k-1} u legs(pi_k)|,
+// dV = the boundary (dense legs) of the absorbed set.  Simulated annealing over single-leaf moves minimises
+// the total; subtree reconfiguration later turns stem segments into small branches where that is cheaper.
+struct Sweep {
+    int NL = 0;
+    std::vector<std::vector<std::pair<int, int>>> nbr;  // per leaf: (other endpoint leaf, edge) per internal leg
+    std::vector<int> deg;                // dense legs per leaf (internal + open)
+    std::vector<uint64_t> q;
+    std::vector<char> sliced;            // per edge
+    double tmax = 1e300;                 // soft bound on every stem size (per slice)
+    int local = 1;                       // sum each sliced edge right after the step that closes it
+    RowModel* rm = nullptr;
+};
+
+struct SweepState {
+    std::vector<int> pi, pos;
+    std::vector<int> B;        // boundary size after position k (sliced legs excluded)
+    std::vector<int> Sk;       // sliced edges touched up to position k (the prefix of the slice order)
+    std::vector<uint64_t> Q;   // fixed-qubit mask after position k
+    std::vector<double> C;     // modelled cost at position k (0 for k = 0), including the peak penalty
+    double total = 0;
+};
+
+// Cost of stem step k over all slices with prefix caching: the step depends on the sliced edges touched so
+// far (S_k of them, the first S_k of the slice order), so it runs 2^S_k times; per run it costs
+// rows * 2^|union| with the sliced legs removed.  Stems above tmax pay a steep penalty.
+inline double sweep_cost(double rows, int uni, int b, int sk, double tmax) {
+    double c = rows * std::ldexp(1.0, uni + sk);
+    const double sz = rows * std::ldexp(1.0, b);
+    if (sz > tmax) c *= 1e6 * (sz / tmax) * (sz / tmax);
+    return c;
+}
+
+// recompute positions lo..hi (inclusive) from the state at lo-1; returns the new sum of C over lo..hi
+inline double sweep_range(const Sweep& S, SweepState& st, int lo, int hi) {
+    int b = lo > 0 ? st.B[lo - 1] : 0;
+    int sk = lo > 0 ? st.Sk[lo - 1] : 0;
+    uint64_t Q = lo > 0 ? st.Q[lo - 1] : 0;
+    double sum = 0;
+    for (int k = lo; k <= hi; k++) {
+        const int v = st.pi[k];
+        int shared = 0, sl_new = 0, sl_deg = 0, sl_close = 0;
+        for (const auto& ue : S.nbr[v]) {
+            if (S.sliced[ue.second]) {
+                sl_deg++;
+                if (st.pos[ue.first] > k) sl_new++;
+                else sl_close++;
+            } else {
+                shared += st.pos[ue.first] < k;
+            }
+        }
+        const int dv = S.deg[v] - sl_deg;
+        const int uni = b + dv - shared;
+        Q |= S.q[v];
+        b = b + dv - 2 * shared;
+        // the step depends on every sliced edge open at it (opened before or at k, closed at or after k); a
+        // sliced edge is summed right after the step that closes it (local slicing), so later steps do not
+        // depend on it.  S.local == 0: flat slicing with prefix caching (touched edges stay)
+        const int dk = sk + sl_new;
+        sk = S.local ? sk + sl_new - sl_close : sk + sl_new;
+        st.B[k] = b;
+        st.Sk[k] = sk;
+        st.Q[k] = Q;
+        st.C[k] = k == 0 ? 0.0 : sweep_cost(S.rm->estimate(Q), uni, b, dk, S.tmax);
+        sum += st.C[k];
+    }
+    return sum;
+}
+
+void sweep_init(const Sweep& S, SweepState& st, const std::vector<int>& pi) {
+    st.pi = pi;
+    st.pos.assign(S.NL, 0);
+    for (int k = 0; k < S.NL; k++) st.pos[pi[k]] = k;
+    st.B.assign(S.NL, 0);
+    st.Sk.assign(S.NL, 0);
+    st.Q.assign(S.NL, 0);
+    st.C.assign(S.NL, 0.0);
+    st.total = sweep_range(S, st, 0, S.NL - 1);
+}
+
+// move the leaf at position i to position j (shifting the ones between)
+inline void sweep_move(SweepState& st, int i, int j) {
+    const int v = st.pi[i];
+    if (i < j)
+        for (int k = i; k < j; k++) { st.pi[k] = st.pi[k + 1]; st.pos[st.pi[k]] = k; }
+    else
+        for (int k = i; k > j; k--) { st.pi[k] = st.pi[k - 1]; st.pos[st.pi[k]] = k; }
+    st.pi[j] = v;
+    st.pos[v] = j;
+}
+
+void sweep_anneal(const Sweep& S, SweepState& st, std::mt19937_64& rng, int64_t iters, double T0, double T1) {
+    std::uniform_real_distribution<double> U(0.0, 1.0);
+    std::vector<int> saveB, saveS;
+    std::vector<uint64_t> saveQ;
+    std::vector<double> saveC;
+    double best_total = st.total;
+    SweepState best = st;
+    for (int64_t it = 0; it < iters; it++) {
+        const double T = T0 * std::pow(T1 / T0, (double)it / (double)iters);
+        const int i = (int)(rng() % (uint64_t)S.NL);
+        const int w = (rng() % 8 == 0) ? S.NL : 12;
+        int j = i + (int)(rng() % (uint64_t)(2 * w + 1)) - w;
+        j = std::max(0, std::min(S.NL - 1, j));
+        if (j == i) continue;
+        const int lo = std::min(i, j), hi = std::max(i, j);
+        double old = 0;
+        for (int k = lo; k <= hi; k++) old += st.C[k];
+        saveB.assign(st.B.begin() + lo, st.B.begin() + hi + 1);
+        saveS.assign(st.Sk.begin() + lo, st.Sk.begin() + hi + 1);
+        saveQ.assign(st.Q.begin() + lo, st.Q.begin() + hi + 1);
+        saveC.assign(st.C.begin() + lo, st.C.begin() + hi + 1);
+        sweep_move(st, i, j);
+        const double nw = sweep_range(S, st, lo, hi);
+        const double newtot = st.total - old + nw;
+        const double d = std::log2(std::max(newtot, 1e-300)) - std::log2(std::max(st.total, 1e-300));
+        if (d <= 0 || U(rng) < std::exp(-d / T)) {
+            st.total = newtot;
+            if (st.total < best_total) {
+                best_total = st.total;
+                best = st;
+            }
+        } else {
+            sweep_move(st, j, i);
+            std::copy(saveB.begin(), saveB.end(), st.B.begin() + lo);
+            std::copy(saveS.begin(), saveS.end(), st.Sk.begin() + lo);
+            std::copy(saveQ.begin(), saveQ.end(), st.Q.begin() + lo);
+            std::copy(saveC.begin(), saveC.end(), st.C.begin() + lo);
+        }
+        if ((it & 0xffff) == 0xffff) st.total = sweep_range(S, st, 0, S.NL - 1);  // drift control
+    }
+    st = best;
+    st.total = sweep_range(S, st, 0, S.NL - 1);
+}
+
+// Checkpointed loop program of a sliced stem (the head/tail "local slices" of P:L131-L136 generalised):
+// checkpoints 0 = p_0 < p_1 < ... < p_J = NL-1 split the stem into segments (p_{j-1}, p_j].  A sliced edge
+// opened at a_e and closed at b_e is looped over by every segment that overlaps [a_e, b_e] and summed at the
+// end of the segment that contains b_e; edges still open in the last segment are the global slices (summed
+// by the readout, split across pipelines and GPUs).  Segment (p, q] runs 2^#{e: a_e <= q, b_e > p} times;
+// the stem at every checkpoint persists across loop iterations (the accumulator at summation points).
+struct Checkpoints {
+    std::vector<int> cp;      // checkpoint positions, cp.back() = NL-1
+    double cost = 0;          // modelled CMAC over all global slices
+    double persist = 0;       // elements persisted at internal checkpoints (one slice iteration)
+};
+
+struct StemEvents {
+    std::vector<double> c;         // per position: rows * 2^|union| of one iteration (sliced legs fixed)
+    std::vector<double> size;      // per position: stem size of one iteration
+    std::vector<std::pair<int, int>> ab;  // per sliced edge: (open position, close position)
+    std::vector<int> edge;         // sliced edge ids (same order)
+};
+
+StemEvents stem_events(const Sweep& S, const SweepState& st, const Network& net, const std::vector<int>& slot_of_tensor) {
+    StemEvents ev;
+    const int NL = S.NL;
+    ev.c.assign(NL, 0.0);
+    ev.size.assign(NL, 0.0);
+    int b = 0;
+    uint64_t Q = 0;
+    for (int k = 0; k < NL; k++) {
+        const int v = st.pi[k];
+        int shared = 0, sl_deg = 0;
+        for (const auto& ue : S.nbr[v]) {
+            if (S.sliced[ue.second]) sl_deg++;
+            else shared += st.pos[ue.first] < k;
+        }
+        const int dv = S.deg[v] - sl_deg;
+        const int uni = b + dv - shared;
+        Q |= S.q[v];
+        b = b + dv - 2 * shared;
+        const double r = S.rm->estimate(Q);
+        ev.c[k] = k == 0 ? 0.0 : r * std::ldexp(1.0, uni);
+        ev.size[k] = r * std::ldexp(1.0, b);
+    }
+    for (int e = 0; e < (int)S.sliced.size(); e++) {
+        if (!S.sliced[e]) continue;
+        const int pa = st.pos[slot_of_tensor[net.edges[e].t0]], pb = st.pos[slot_of_tensor[net.edges[e].t1]];
+        ev.ab.push_back({std::min(pa, pb), std::max(pa, pb)});
+        ev.edge.push_back(e);
+    }
+    return ev;
+}
+
+// exact DP over checkpoint sets with at most J segments; persisted memory is charged lambda CMAC per element
+Checkpoints checkpoint_dp(const StemEvents& ev, int J, double lambda) {
+    const int K = (int)ev.c.size();
+    std::vector<double> pre(K + 1, 0.0);
+    for (int k = 0; k < K; k++) pre[k + 1] = pre[k] + ev.c[k];
+    auto seg = [&](int p, int q) {  // steps p+1..q; edges with a <= q and b > p
+        int n = 0;
+        double acc = 0;
+        for (const auto& x : ev.ab) {
+            if (x.first <= q && x.second > p) {
+                n++;
+                if (x.second <= q && q < K - 1) acc = 1;  // a summation at q (an accumulate pass)
+            }
+        }
+        return (pre[q + 1] - pre[p + 1] + acc * 3 * ev.size[q]) * std::ldexp(1.0, n);
+    };
+    const double INF = 1e308;
+    std::vector<std::vector<double>> D(J + 1, std::vector<double>(K, INF));
+    std::vector<std::vector<int>> arg(J + 1, std::vector<int>(K, -1));
+    D[0][0] = 0;
+    for (int j = 1; j <= J; j++)
+        for (int q = 1; q < K; q++)
+            for (int p = 0; p < q; p++) {
+                if (D[j - 1][p] >= INF) continue;
+                const double v = D[j - 1][p] + seg(p, q) + (p > 0 ? lambda * ev.size[p] : 0.0);
+                if (v < D[j][q]) {
+                    D[j][q] = v;
+                    arg[j][q] = p;
+                }
+            }
+    Checkpoints best;
+    best.cost = INF;
+    int bj = -1;
+    for (int j = 1; j <= J; j++)
+        if (D[j][K - 1] < best.cost) {
+            best.cost = D[j][K - 1];
+            bj = j;
+        }
+    for (int q = K - 1, j = bj; j > 0; q = arg[j][q], j--) best.cp.push_back(q);
+    std::reverse(best.cp.begin(), best.cp.end());
+    best.cost = 0;
+    best.persist = 0;
+    int p = 0;
+    for (int q : best.cp) {
+        best.cost += seg(p, q);
+        if (q < K - 1) best.persist += ev.size[q];
+        p = q;
+    }
+    return best;
+}
+
+Tree sweep_tree(const std::vector<Leaf>& leaves, const std::vector<int>& pi, RowModel& rm) {
+    const int NL = (int)leaves.size();
+    Tree t;
+    t.nodes.resize(NL);
+    for (int i = 0; i < NL; i++) {
+        Node& N = t.nodes[i];
+        N.leaf = i;
+        for (int e : leaves[i].legs) N.legs.set(e);
+        N.q = leaves[i].qmask;
+        N.rows = (double)leaves[i].rows.size();
+    }
+    int cur = pi[0];
+    for (int k = 1; k < NL; k++) {
+        Node N;
+        N.left = cur;
+        N.right = pi[k];
+        N.legs = t.nodes[cur].legs ^ t.nodes[pi[k]].legs;
+        N.q = t.nodes[cur].q | t.nodes[pi[k]].q;
+        N.rows = rm.rows(N.q);
+        const int id = (int)t.nodes.size();
+        t.nodes[cur].parent = id;
+        t.nodes[pi[k]].parent = id;
+        t.nodes.push_back(N);
+        cur = id;
+    }
+    t.root = cur;
+    return t;
+}
+
+// leaves of a tree in depth-first order (a nested-dissection linear order for rb2 trees)
+std::vector<int> leaf_order(const Tree& t) {
+    std::vector<int> out, st = {t.root};
+    while (!st.empty()) {
+        const int x = st.back();
+        st.pop_back();
+        const Node& N = t.nodes[x];
+        if (N.leaf >= 0) { out.push_back(N.leaf); continue; }
+        st.push_back(N.right);
+        st.push_back(N.left);
+    }
+    return out;
+}
+
 // emit (i, j) pairs with the result stored at i (SPEC.md S:L252 convention)
 std::vector<std::pair<int, int>> tree_order(const Tree& t) {
     std::vector<std::pair<int, int>> out;
@@ -587,6 +989,213 @@ std::vector<std::pair<int, int>> tree_order(const Tree& t) {
         }
     }
     return out;
+}
+
+// The loop-program planner (method 2): stem sweeps with local slicing and checkpointed segments.
+//   1. multilevel-bisection trees give nested-dissection leaf orders;
+//   2. each order is annealed as a stem (sweep_anneal), then sliced edge by edge under max_elems with the
+//      local-summation cost model, re-annealing after every slice;
+//   3. checkpoint_dp picks <= max_segments segments under the persistence budget;
+//   4. the best program by modelled CMAC becomes the plan (order = the stem, segments, global/local bits).
+std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, const Request& req, const PlanOptions& opt,
+                       const std::vector<int>& internal, const std::vector<int>& slot_of_tensor, RowModel& rm,
+                       std::mt19937_64& rng, double budget, Plan& out) {
+    static const bool verbose = getenv("TNB_PLAN_VERBOSE") != nullptr;
+    const int NL = (int)leaves.size();
+    auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&]() { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    Bits none;
+    // ---------------- 1. bisection trees (their leaf orders seed the sweeps)
+    RB2 P{&leaves, &net, &slot_of_tensor, &internal, &rm, 0.0, 0.0, 0, 0, 0.0};
+    std::vector<std::pair<double, Tree>> hp;
+    const double L2 = std::log2(std::max<double>(1.0, (double)req.fixed.size()));
+    const int rb_trials = std::max(4, opt.trials > 0 ? opt.trials : 64);
+    for (int trial = 0; trial < rb_trials && (trial < 4 || elapsed() < 0.25 * budget); trial++) {
+        P.eps_lo = std::vector<double>{0.01, 0.05, 0.1, 0.2}[rng() % 4];
+        P.eps_hi = P.eps_lo + std::vector<double>{0.0, 0.1, 0.3, 0.6}[rng() % 4];
+        P.cutoff = 2 + (int)(rng() % 12);
+        P.rows_w = (int)std::lround(L2 * std::vector<double>{0.0, 0.25, 0.5, 1.0, 2.0}[rng() % 5]);
+        P.fix_ext = 0.0;
+        Tree t = rb2_tree(P, rng);
+        TreeEval ev = eval_tree(t, none);
+        hp.push_back({ev.cmac, std::move(t)});
+    }
+    std::sort(hp.begin(), hp.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    // ---------------- 2. sweeps
+    Sweep S;
+    S.NL = NL;
+    S.rm = &rm;
+    S.nbr.resize(NL);
+    S.deg.resize(NL);
+    S.q.resize(NL);
+    S.sliced.assign(net.edges.size(), 0);
+    for (int i = 0; i < NL; i++) {
+        S.deg[i] = (int)leaves[i].legs.size();
+        S.q[i] = leaves[i].qmask;
+    }
+    for (int e : internal) {
+        const int a = slot_of_tensor[net.edges[e].t0], b = slot_of_tensor[net.edges[e].t1];
+        S.nbr[a].push_back({b, e});
+        S.nbr[b].push_back({a, e});
+    }
+    const int64_t iters = opt.sweep_iters > 0 ? opt.sweep_iters : std::max<int64_t>(20000, (int64_t)NL * 4000);
+    const double pbudget = opt.persist_budget > 0 ? opt.persist_budget : 8.0 * opt.max_elems;
+    auto peak_of = [&](const SweepState& x) {
+        double pk = 0;
+        for (int i = 0; i < NL; i++) pk = std::max(pk, rm.estimate(x.Q[i]) * std::ldexp(1.0, x.B[i]));
+        return pk;
+    };
+    bool have = false;
+    double best_cost = 1e308;
+    SweepState best_st;
+    std::vector<char> best_sliced;
+    Checkpoints best_cp;
+    StemEvents best_ev;
+    for (int k = 0; k < (int)hp.size() && (k < 2 || elapsed() < budget); k++) {
+        std::fill(S.sliced.begin(), S.sliced.end(), 0);
+        for (int e : opt.forced) S.sliced[e] = 1;
+        S.tmax = 1e300;
+        SweepState st;
+        sweep_init(S, st, leaf_order(hp[k].second));
+        sweep_anneal(S, st, rng, iters, 0.5, 0.01);
+        S.tmax = opt.max_elems;
+        bool ok = true;
+        for (int ns = 0;; ns++) {
+            st.total = sweep_range(S, st, 0, NL - 1);
+            if (peak_of(st) <= opt.max_elems) break;
+            if (ns >= 62) { ok = false; break; }
+            std::vector<char> cand(net.edges.size(), 0);
+            for (int i = 0; i < NL; i++) {
+                if (rm.estimate(st.Q[i]) * std::ldexp(1.0, st.B[i]) <= opt.max_elems) continue;
+                for (int j = 0; j <= i; j++)
+                    for (const auto& ue : S.nbr[st.pi[j]])
+                        if (!S.sliced[ue.second] && st.pos[ue.first] > i) cand[ue.second] = 1;
+            }
+            int be = -1;
+            double bt = 1e308;
+            SweepState tmp = st;
+            for (int e : internal) {
+                if (!cand[e]) continue;
+                S.sliced[e] = 1;
+                const double tt = sweep_range(S, tmp, 0, NL - 1);
+                S.sliced[e] = 0;
+                if (tt < bt) { bt = tt; be = e; }
+            }
+            if (be < 0) { ok = false; break; }
+            S.sliced[be] = 1;
+            st.total = sweep_range(S, st, 0, NL - 1);
+            sweep_anneal(S, st, rng, iters / 8, 0.2, 0.01);
+        }
+        if (!ok) continue;
+        // leaves larger than the bound cannot be sliced further by this planner
+        StemEvents sev = stem_events(S, st, net, slot_of_tensor);
+        Checkpoints c;
+        for (double lambda = 0.0;; lambda = lambda > 0 ? lambda * 4 : 1e-3) {
+            c = checkpoint_dp(sev, std::max(1, opt.max_segments), lambda);
+            if (c.persist <= pbudget || lambda > 1e12) break;
+        }
+        if (c.persist > pbudget) continue;
+        if (verbose)
+            fprintf(stderr, "[plan] sweep %d: s %zu, %zu segments, cost %.3e, persist 2^%.1f, peak 2^%.1f (%.1f s)\n", k,
+                    sev.edge.size(), c.cp.size(), c.cost, std::log2(std::max(1.0, c.persist)), std::log2(peak_of(st)),
+                    elapsed());
+        if (!have || c.cost < best_cost) {
+            have = true;
+            best_cost = c.cost;
+            best_st = st;
+            best_sliced = S.sliced;
+            best_cp = c;
+            best_ev = sev;
+        }
+    }
+    if (!have) return "the loop-program planner found no plan within max_tensor_size and the persistence budget";
+    // ---------------- 3. the plan: stem order, bits, segments
+    Plan pl;
+    Tree t = sweep_tree(leaves, best_st.pi, rm);
+    pl.order = tree_order(t);
+    const std::vector<int>& cp = best_cp.cp;
+    const int J = (int)cp.size();
+    auto seg_of_pos = [&](int pos) {
+        int j = 0;
+        while (cp[j] < pos) j++;
+        return j;
+    };
+    pl.step_seg.resize(pl.order.size());
+    for (size_t p = 0; p < pl.order.size(); p++) pl.step_seg[p] = seg_of_pos((int)p + 1);
+    // summation segment of each sliced edge: the segment containing its close position; the last segment's
+    // edges are global
+    const int ns = (int)best_ev.edge.size();
+    std::vector<int> sumseg(ns);
+    for (int i = 0; i < ns; i++) sumseg[i] = seg_of_pos(best_ev.ab[i].second);
+    // at least opt.n_sliced global bits (parallel slices): promote the latest-summed local edges
+    {
+        int ng = 0;
+        for (int i = 0; i < ns; i++) ng += sumseg[i] == J - 1;
+        while (ng < opt.n_sliced && ng < ns) {
+            int bi = -1;
+            for (int i = 0; i < ns; i++)
+                if (sumseg[i] < J - 1 && (bi < 0 || sumseg[i] > sumseg[bi])) bi = i;
+            sumseg[bi] = J - 1;
+            ng++;
+        }
+    }
+    std::vector<int> idx(ns);
+    for (int i = 0; i < ns; i++) idx[i] = i;
+    // bit order: global first (MSB), then local by summation segment descending (earliest summed = LSB)
+    std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return sumseg[x] > sumseg[y]; });
+    pl.n_global = 0;
+    for (int i : idx) {
+        pl.sliced.push_back(best_ev.edge[i]);
+        if (sumseg[i] == J - 1) pl.n_global++;
+    }
+    auto bit = [&](int rank) { return 1ull << (ns - 1 - rank); };
+    pl.segs.resize(J);
+    for (int j = 0; j < J; j++) {
+        const int p = j == 0 ? 0 : cp[j - 1], q = cp[j];
+        for (int r = 0; r < ns; r++) {
+            const int i = idx[r];
+            const auto& ab = best_ev.ab[i];
+            const int close = sumseg[i] == J - 1 ? NL - 1 : ab.second;  // promoted globals stay open
+            if (ab.first <= q && close > p) pl.segs[j].D |= bit(r);
+            if (sumseg[i] == j && j < J - 1) pl.segs[j].E |= bit(r);
+        }
+        for (int jj = 0; jj < j; jj++) pl.segs[j].Sum |= pl.segs[jj].E;
+    }
+    // modelled cost of the program (promotions included)
+    {
+        double tot = 0;
+        for (int j = 0; j < J; j++) {
+            const int p = j == 0 ? 0 : cp[j - 1], q = cp[j];
+            double c = 0;
+            for (int k = p + 1; k <= q; k++) c += best_ev.c[k];
+            if (pl.segs[j].E) c += 3 * best_ev.size[q];
+            tot += c * std::ldexp(1.0, __builtin_popcountll(pl.segs[j].D));
+        }
+        pl.total_cmac = tot;
+    }
+    pl.persist_elems = best_cp.persist;
+    TreeEval ev = eval_tree(t, Bits());
+    (void)ev;
+    // per-iteration figures of the sliced network (cmac of one pass over every step)
+    {
+        double c = 0, pk = 0;
+        for (int k = 0; k < NL; k++) {
+            c += best_ev.c[k];
+            pk = std::max(pk, best_ev.size[k]);
+        }
+        pl.cmac = c;
+        pl.peak = pk;
+    }
+    if (verbose) {
+        fprintf(stderr, "[plan] loop program: %d global + %d local bits, %d segments, total %.3e CMAC, persist 2^%.1f\n",
+                pl.n_global, ns - pl.n_global, J, pl.total_cmac, std::log2(std::max(1.0, pl.persist_elems)));
+        for (int j = 0; j < J; j++)
+            fprintf(stderr, "[plan]   seg %d: steps ..%d  |D| %d  |Sum| %d  |E| %d\n", j, cp[j],
+                    __builtin_popcountll(pl.segs[j].D), __builtin_popcountll(pl.segs[j].Sum),
+                    __builtin_popcountll(pl.segs[j].E));
+    }
+    out = pl;
+    return "";
 }
 
 }  // namespace
@@ -627,6 +1236,11 @@ std::string find_plan(const Network& net, const std::vector<Leaf>& leaves, const
     auto t0 = std::chrono::steady_clock::now();
     auto elapsed = [&]() { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
 
+    const int method = opt.method != 0 ? opt.method : (NL > 160 ? 2 : 1);
+    if (method == 2) {
+        if (!opt.companions.empty()) return "companion edges are not supported by the loop-program planner";
+        return sweep_plan(net, leaves, req, opt, internal, slot_of_tensor, rm, rng, budget, out);
+    }
     // ---------------- 1. greedy trees; keep the best few by unsliced modelled time
     std::vector<std::pair<double, Tree>> pool;
     Bits none;
@@ -654,7 +1268,9 @@ std::string find_plan(const Network& net, const std::vector<Leaf>& leaves, const
             g.adj[kv.first.second].push_back({kv.first.first, kv.second});
         }
     }
-    const int rb_trials = NL > 24 ? std::max(8, trials) : 0;
+    const bool hyper = false;
+    static const bool verbose = getenv("TNB_PLAN_VERBOSE") != nullptr;
+    const int rb_trials = (NL > 24 && !hyper) ? std::max(8, trials) : 0;
     for (int trial = 0; trial < rb_trials; trial++) {
         if (trial >= 2 && elapsed() > 0.45 * budget) break;
         const double eps = std::vector<double>{0.1, 0.3, 0.5, 0.2, 0.05, 0.4}[trial % 6];
@@ -690,6 +1306,11 @@ std::string find_plan(const Network& net, const std::vector<Leaf>& leaves, const
             s++;
         }
         pt.first = std::ldexp(eval_tree(pt.second, S).time, s);
+        if (verbose) {
+            TreeEval e0 = eval_tree(pt.second, none), e1 = eval_tree(pt.second, S);
+            fprintf(stderr, "[plan] pool: unsliced cmac %.3e peak 2^%.1f -> s %d total cmac %.3e time %.3e s\n", e0.cmac,
+                    std::log2(e0.peak), s, std::ldexp(e1.cmac, s), pt.first);
+        }
     }
     std::sort(pool.begin(), pool.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
     const int keep = std::min<int>((int)pool.size(), 3);

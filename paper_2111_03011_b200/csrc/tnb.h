@@ -4,7 +4,9 @@
 
 #include <complex>
 #include <cstdint>
+#include <random>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/tn.h"
@@ -99,6 +101,21 @@ struct Plan {
     std::vector<std::pair<int, int>> tied_wire;  // (q, k): the projector's wire, right before the gate
     double cmac = 0, bytes = 0, time_s = 0;  // per slice
     double peak = 0;                         // elements, per slice
+    // Loop program (head/tail local slices; planner.cpp checkpoint_dp).  Empty `segs`: flat
+    // slicing, every sliced edge is a slice-id bit.  Otherwise the first n_global entries of `sliced` are the
+    // slice-id bits (global slices, summed by the readout) and the rest are local loop bits summed inside the
+    // program.  Loop index tau has s = sliced.size() bits, sliced[i] <-> tau bit (s-1-i); tau = (sigma <<
+    // (s - n_global)) | local.  Pairwise step p belongs to segment step_seg[p] (nondecreasing); a segment runs
+    // at tau iff all its Sum bits are 1 and its D bits differ from its previous run; E = local bits summed
+    // (accumulated) at the end of the segment.
+    int n_global = -1;
+    std::vector<int> step_seg;
+    struct Seg {
+        uint64_t D = 0, Sum = 0, E = 0;
+    };
+    std::vector<Seg> segs;
+    double total_cmac = 0;   // modelled CMAC of the whole loop program over all global slices
+    double persist_elems = 0;
 };
 
 // Companion-edge rank-one truncation (supplement "singular values of the sliced fSim gate"):
@@ -123,17 +140,40 @@ struct PlanOptions {
     int trials = 0;
     double time_budget_s = 0;
     double max_elems = 0;
+    int hyper = -1;
+    int64_t sweep_iters = 0;   // annealing moves per sweep order (0: default)
+    int method = 0;            // 0 auto, 1 flat slicing (greedy/bisection pool), 2 sweep loop program
+    int max_segments = 8;      // loop program: at most this many segments
+    double persist_budget = 0; // loop program: elements persisted across iterations (0: 8 x max_elems)            // multilevel-bisection tree search: 1 on, 0 off, -1 auto (> 160 leaves)
 };
 
 // row-count oracle used by the planner (exact with memo for small L, estimate otherwise)
 struct RowModel {
     const Request* req = nullptr;
     double rows(uint64_t qmask);
-    std::vector<std::pair<uint64_t, double>> memo;
+    double estimate(uint64_t qmask) const;
+    std::unordered_map<uint64_t, double> memo;
 };
+
+// A hypergraph for the partitioner (partition.cpp): nodes with weights, nets (pin lists) with weights.
+struct HyperGraph {
+    int n = 0;
+    std::vector<int> node_w;
+    std::vector<std::vector<int>> nets;
+    std::vector<int> net_w;
+    std::vector<int8_t> fixed;  // empty, or per node: -1 free, 0 / 1 fixed to that side
+};
+// Multilevel min-cut bisection: side[v] in {0, 1}, each side's node weight within (1/2 +- eps/2) * total
+// when reachable.  init_tries greedy-growing starts at the coarsest level.
+std::vector<char> ml_bisect(const HyperGraph& g, double eps, std::mt19937_64& rng, int init_tries);
 
 std::string find_plan(const Network& net, const std::vector<Leaf>& leaves, const Request& req,
                       const PlanOptions& opt, Plan& out);
+
+// Plan files (planfile.cpp): the order by tensor id, sliced wires (q, k) in bit
+// order, n_global, step segments and the segment masks.  load_plan validates the file against the network.
+std::string save_plan(const Network& net, const std::vector<Leaf>& leaves, const Plan& plan, const std::string& path);
+std::string load_plan(const Network& net, const std::vector<Leaf>& leaves, const std::string& path, Plan& plan);
 
 // ---------------------------------------------------------------------------- lowered program
 
@@ -144,7 +184,7 @@ struct BitMap {
     int8_t dst[40];
 };
 
-enum BufRegion : int32_t { REG_NONE = 0, REG_WORK = 1, REG_BANK = 2, REG_MAPS = 3, REG_PERS = 4 };
+enum BufRegion : int32_t { REG_NONE = 0, REG_WORK = 1, REG_BANK = 2, REG_MAPS = 3, REG_PERS = 4, REG_LVL = 5 };
 struct BufRef {
     int32_t region = REG_NONE;
     int64_t offset = 0;   // bytes
@@ -158,7 +198,9 @@ enum StepKind : int32_t {
     K_GEMM = 4,
     K_READOUT = 5,
     K_PERMUTE = 6,
-    K_MULTI = 7
+    K_MULTI = 7,
+    K_ACCUM = 8,      // loop program: dst = ((tau & E) == 0 ? 0 : dst) + src (local-slice summation)
+    K_SETTAU = 9      // (executor-internal)
 };
 
 // General sparse-row pairwise contraction (SIMT path):
@@ -217,6 +259,12 @@ struct InstParams {
     int32_t n_leaves = 0;
 };
 
+struct AccumParams {
+    BufRef src, dst;
+    int64_t n = 0;            // complex elements
+    uint64_t E = 0;           // tau bits summed here: the first value (all zero) overwrites
+};
+
 struct ReadoutParams {
     BufRef F;                 // final tensor
     BufRef idx;               // REG_MAPS: int64 index per amplitude
@@ -240,6 +288,7 @@ struct Step {
     GemmParams gp;
     InstParams ip;
     ReadoutParams rp;
+    AccumParams cp;
 };
 
 // device-side descriptor of one sliced leaf for K_INSTANTIATE (slice instantiate, row a2)
@@ -267,6 +316,15 @@ struct Program {
     int64_t n_pairs = 0;
     // per-leaf slicing info for K_INSTANTIATE (also in `maps`)
     int s = 0;
+    // loop program (Plan::segs): per segment the run condition and its steps; empty = flat (`steps`)
+    struct Seg {
+        uint64_t D = 0, Sum = 0, E = 0;
+        std::vector<Step> steps;
+    };
+    std::vector<Seg> segs;
+    int s_global = 0;          // slice-id bits (the top bits of the loop index)
+    int64_t lvl_bytes = 0;     // REG_LVL: tensors kept across loop iterations (checkpoints, accumulators)
+    double total_cmac = 0;     // over all 2^s_global slices, counting each segment's runs
     // plan dump support
     std::string dump_json;
 };

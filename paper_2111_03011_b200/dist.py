@@ -32,13 +32,40 @@ def allreduce_amplitudes(amps, group=None):
     return amps
 
 
-def contract_distributed(ss, slice_ids: Sequence[int], out=None):
+def plan_fingerprint(info: dict) -> str:
+    """Identity of a plan as the slice-id space sees it: the global and local sliced wires, the segment count
+    and the step count.  Ranks that sum partial amplitudes must hold the same plan (else the all-reduce adds
+    slices of different networks)."""
+    import hashlib
+    key = repr((info["s"], info["sliced_wires"], info.get("s_local", 0), info.get("local_wires", []),
+                info.get("n_segments", 1), info["n_steps"], info["n_tensors"]))
+    return hashlib.sha256(key.encode()).hexdigest()
+
+
+def check_same_plan(info: dict, group=None) -> None:
+    """All-gather the plan fingerprint and raise if any rank planned differently (the planner's search is
+    time-budgeted, so independent searches may differ: plan once and import the plan file instead)."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    fp = plan_fingerprint(info)
+    allfp = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allfp, fp, group=group)
+    if len(set(allfp)) != 1:
+        raise RuntimeError(f"ranks hold different plans (fingerprints {sorted(set(allfp))}); plan on one rank, "
+                           "save_plan(), and load it with plan(plan_path=...) on every rank")
+
+
+def contract_distributed(ss, slice_ids: Sequence[int], out=None, check_plan: bool = True):
     """Each rank contracts its block of slice_ids on its own GPU (tn_contract), then all ranks
-    all-reduce.  Returns the summed amplitudes (complex64 CUDA tensor) on every rank."""
+    all-reduce.  Returns the summed amplitudes (complex64 CUDA tensor) on every rank.  The ranks'
+    plans are compared first (check_same_plan)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size() if dist.is_initialized() else 1
     rank = dist.get_rank() if dist.is_initialized() else 0
+    if check_plan:
+        check_same_plan(ss.info)
     block = partition(slice_ids, world, rank)
     if out is None:
         out = torch.empty(ss.M, dtype=torch.complex64, device=torch.device("cuda", ss._dev))

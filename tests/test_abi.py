@@ -161,6 +161,10 @@ def test_plan_rows_bit_exact(T, tmp_path, k):
     Qf = qubits(fin["qmask"])
     assert sorted(Qf) == sorted(set(range(n)) - set(c.open_ids(n)))
     np.testing.assert_array_equal(rows.project(np.array(fin["row_keys"], np.uint64), n, Qf), rows.rows(bits, n, Qf))
+    # readout: amplitude j reads the final row holding its fixed part
+    keys = np.array(fin["row_keys"], np.uint64)
+    mask = np.uint64(fin["qmask"])
+    np.testing.assert_array_equal(keys[rows.readout_rows(bits, n, Qf)], bits & mask)
 
 
 def test_mac_count_identity(T, tmp_path):

@@ -260,6 +260,26 @@ def test_paper_three_qubit_example():
     assert [format(int(v), "03b") for v in rows.rows(req, 3, [0, 1, 2])] == lines["final_rows"].split()
 
 
+def test_readout_rows_paper_example_and_bruteforce():
+    """readout_rows: PAPER.md L202's request {111, 010, 000} reads rows {000, 010, 111} -> [2, 1, 0]; and on a
+    random grouped request every amplitude's row holds its projection, computed bit by bit here."""
+    from oracle import rows
+    req = np.array([0b111, 0b010, 0b000], np.uint64)
+    np.testing.assert_array_equal(rows.readout_rows(req, 3, [0, 1, 2]), [2, 1, 0])
+    np.testing.assert_array_equal(rows.readout_rows(req, 3, [1, 2]), [2, 1, 0])   # rows {00, 10, 11}
+    np.testing.assert_array_equal(rows.readout_rows(req, 3, [0]), [1, 0, 0])      # rows {0, 1}
+    n = 9
+    x = bs.generate_groups(n, [7, 8], 30, 11)
+    Q = [0, 2, 3, 6]
+    table = rows.rows(x, n, Q)
+    idx = rows.readout_rows(x, n, Q)
+    for j, b in enumerate(x):
+        key = 0
+        for q in Q:
+            key = 2 * key + ((int(b) >> (n - 1 - q)) & 1)
+        assert int(table[idx[j]]) == key
+
+
 def test_rows_full_request_is_dense():
     """request = all 2^n bitstrings degenerates to the dense case."""
     from oracle import rows
@@ -298,6 +318,24 @@ def test_fidelity_definitions(oracle_built):
     orth[(i + 1) % len(psi)] = np.conj(psi[i])
     assert metrics.f_exact(psi, orth) < 1e-25
     assert abs(metrics.f_norm(psi, 6) - 1) < 1e-12                            # full request, exact state
+
+
+def test_f_sparse_closed_forms(oracle_built):
+    """SURVEY §8(c) item 16: F_sparse(a, b) = |sum a_j^* b_j|^2 / (sum |a_j|^2 sum |b_j|^2).  Identity -> 1;
+    global phase and scale -> 1; orthogonal -> 0; hand-worked 2-vectors; on a full request it is F_exact."""
+    from oracle import metrics, sv
+    a = np.array([1.0, 0.0], complex)
+    assert abs(metrics.f_sparse(a, np.array([1.0, 1.0])) - 0.5) < 1e-15          # |1|^2 / (1 * 2)
+    assert abs(metrics.f_sparse(np.array([1.0, 1j]), np.array([1.0, 1.0])) - 0.5) < 1e-15  # |1 - i|^2 / 4
+    assert abs(metrics.f_sparse(np.array([3.0, 4.0]), np.array([4.0, -3.0]))) < 1e-15     # orthogonal
+    # a = (1, 2i), b = (2, i): sum a^* b = 2 + (-2i)(i) = 4; |4|^2 / (5 * 5) = 16/25
+    assert abs(metrics.f_sparse(np.array([1.0, 2j]), np.array([2.0, 1j])) - 0.64) < 1e-15
+    psi = sv.statevector(small_circuit(2, 3, 4, 43))
+    amps = psi[:17]
+    assert abs(metrics.f_sparse(amps, amps) - 1) < 1e-12
+    assert abs(metrics.f_sparse(amps, 0.3 * np.exp(-1.1j) * amps) - 1) < 1e-12
+    phi = sv.statevector(small_circuit(2, 3, 4, 44))
+    assert abs(metrics.f_sparse(psi, phi) - metrics.f_exact(psi, phi)) < 1e-12
 
 
 def test_xeb_uniform_and_exact(oracle_built):

@@ -1,5 +1,6 @@
 """Throughput of variants with concurrent pipelines: each argument is "VAR=val;VAR2=val" env settings read at
-bind (e.g. TNB_SKIP=k1 drops launch kind 1: outputs are then wrong, timing only)."""
+bind (e.g. TNB_SKIP=k1 drops launch kind 1: outputs are then wrong, timing only).  Needs a diagnostics build:
+TNB_NVCC_FLAGS=-DTNB_DIAG_SKIP python -m paper_2111_03011_b200.build (the product build ignores TNB_SKIP)."""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
