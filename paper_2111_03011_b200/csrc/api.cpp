@@ -200,7 +200,8 @@ tn_status tn_plan(tn_ctx* ctx, const tn_slicing* slicing, int64_t max_tensor_siz
     const int s_glob = plan.segs.empty() ? s_all : plan.n_global;
     for (int i = 0; i < s_all; i++) {
         const int eid = plan.sliced[i];
-        auto& v = i < s_glob ? ctx->sliced_wires : ctx->local_wires;
+        const bool g = plan.segs.empty() || plan.is_global[i];
+        auto& v = g ? ctx->sliced_wires : ctx->local_wires;
         v.push_back(ctx->net.edges[eid].q);
         v.push_back(ctx->net.edges[eid].k);
     }

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -174,6 +175,7 @@ struct Device {
         uint64_t D, Sum, E;
     };
     std::vector<SegMask> segm;       // empty: flat program (one graph per slice)
+    std::vector<char> bit_global;    // loop program: per tau bit, MSB first (1 = slice-id bit)
     std::vector<cudaStream_t> capture_streams;  // fork streams used while capturing the graphs (DAG)
 };
 
@@ -1304,6 +1306,7 @@ int dev_bind(Device** out, const Program& prog, int device, void* workspace, siz
     }
     d->s_global = prog.segs.empty() ? prog.s : prog.s_global;
     for (const auto& g : prog.segs) d->segm.push_back({g.D, g.Sum, g.E});
+    d->bit_global = prog.bit_global;
     d->pipes.resize(np);
     for (int p = 0; p < np; p++) {
         Pipe& P = d->pipes[p];
@@ -1395,48 +1398,68 @@ int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_ou
             }
         }
     } else {
-        // loop program: tau = sigma << l | local runs through the local values of every slice in order; a
-        // segment runs when all its Sum bits are 1 (the summations it reads are complete) and its D bits
-        // differ from its previous run (otherwise its kept outputs are still valid: head reuse)
-        const int l = d->s - d->s_global;
-        const int J = (int)d->segm.size();
-        struct It {
-            int64_t i = 0;
-            std::vector<uint64_t> last;
-            std::vector<char> ran;
+        // loop program: every pipeline enumerates the loop index tau in increasing order, its global bits
+        // restricted to the pipeline's block of slice ids (a trie walk over the sorted block; global and
+        // local bits may interleave in significance); a segment runs when all its Sum bits are 1 (the
+        // summations it reads are complete) and its D bits differ from its previous run (else its kept
+        // outputs are still valid: head reuse).  Launches are issued round-robin over the pipelines.
+        const int s = d->s, J = (int)d->segm.size();
+        std::vector<int> gpos(s, -1);  // tau bit index (MSB first) -> global ordinal
+        int ng = 0;
+        for (int i = 0; i < s; i++)
+            if (d->bit_global[i]) gpos[i] = ng++;
+        struct Item {
+            uint64_t tau;
+            int seg;
+            bool set;
         };
-        std::vector<It> its(np);
+        std::vector<std::vector<Item>> lists(np);
         for (int p = 0; p < np; p++) {
-            its[p].last.assign(J, 0);
-            its[p].ran.assign(J, 0);
-        }
-        bool more = true;
-        while (more) {  // round-robin over pipelines, one slice at a time
-            more = false;
-            for (int p = 0; p < np; p++) {
-                if (its[p].i >= pcnt[p]) continue;
-                Pipe& P = d->pipes[p];
-                const uint64_t sigma = ids_sorted[pstart[p] + its[p].i];
-                for (uint64_t loc = 0; loc < (1ull << l); loc++) {
-                    const uint64_t tau = (sigma << l) | loc;
+            if (pcnt[p] == 0) continue;
+            const uint64_t* blk = ids_sorted + pstart[p];
+            std::vector<uint64_t> last(J, 0);
+            std::vector<char> ran(J, 0);
+            std::vector<Item>& out = lists[p];
+            std::function<void(int, uint64_t, int64_t, int64_t)> walk = [&](int i, uint64_t tau, int64_t lo, int64_t hi) {
+                if (i == s) {
                     bool set = false;
                     for (int j = 0; j < J; j++) {
                         const Device::SegMask& g = d->segm[j];
                         if ((tau & g.Sum) != g.Sum) continue;
                         const uint64_t dv = tau & g.D;
-                        if (its[p].ran[j] && its[p].last[j] == dv) continue;
-                        if (!set) {
-                            kern::k_set_tau<<<1, 1, 0, P.stream>>>(P.tau, tau);
-                            set = true;
-                        }
-                        CK(cudaGraphLaunch(P.seg[j].gexec, P.stream));
-                        its[p].ran[j] = 1;
-                        its[p].last[j] = dv;
+                        if (ran[j] && last[j] == dv) continue;
+                        out.push_back({tau, j, !set});
+                        set = true;
+                        ran[j] = 1;
+                        last[j] = dv;
                     }
+                    return;
                 }
-                its[p].i++;
-                more = more || its[p].i < pcnt[p];
+                const uint64_t bit = 1ull << (s - 1 - i);
+                if (gpos[i] < 0) {
+                    walk(i + 1, tau, lo, hi);
+                    walk(i + 1, tau | bit, lo, hi);
+                    return;
+                }
+                const int sh = ng - 1 - gpos[i];  // the block entries in [lo, hi) agree on the higher global bits
+                int64_t mid = lo;
+                while (mid < hi && !((blk[mid] >> sh) & 1)) mid++;
+                if (mid > lo) walk(i + 1, tau, lo, mid);
+                if (hi > mid) walk(i + 1, tau | bit, mid, hi);
+            };
+            walk(0, 0, 0, pcnt[p]);
+        }
+        for (size_t k = 0;; k++) {
+            bool any = false;
+            for (int p = 0; p < np; p++) {
+                if (k >= lists[p].size()) continue;
+                any = true;
+                const Item& it = lists[p][k];
+                Pipe& P = d->pipes[p];
+                if (it.set) kern::k_set_tau<<<1, 1, 0, P.stream>>>(P.tau, it.tau);
+                CK(cudaGraphLaunch(P.seg[it.seg].gexec, P.stream));
             }
+            if (!any) break;
         }
     }
     for (int p = 0; p < np; p++)
@@ -1494,7 +1517,12 @@ int dev_profile(Device* d, uint64_t slice_id, tn_launch_stat* stats, int max_sta
         CK(cudaMemcpyAsync(P.slice_ids, &slice_id, sizeof(uint64_t), cudaMemcpyHostToDevice, P.stream));
         for (const Launch& L : P.launches) seq.push_back({&P, &L});
     } else {
-        const uint64_t tau = slice_id << (d->s - d->s_global);
+        uint64_t tau = 0;  // the slice id's bits at the global positions, local bits 0
+        for (int i = 0, gk = 0; i < d->s; i++)
+            if (d->bit_global[i]) {
+                if ((slice_id >> (d->s_global - 1 - gk)) & 1) tau |= 1ull << (d->s - 1 - i);
+                gk++;
+            }
         kern::k_set_tau<<<1, 1, 0, P.stream>>>(P.tau, tau);
         for (Pipe& C : P.seg)
             for (const Launch& L : C.launches) seq.push_back({&C, &L});

@@ -111,9 +111,19 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             prog.segs[j].E = plan.segs[j].E;
             if (plan.segs[j].E & ~plan.segs[j].D) return "loop program: a segment sums a bit it does not loop over";
         }
-        const uint64_t local = (s - plan.n_global) >= 64 ? ~0ull : ((1ull << (s - plan.n_global)) - 1);
+        if ((int)plan.is_global.size() != s) return "loop program: is_global length differs from the sliced list";
+        uint64_t local = 0;
+        int ng = 0;
+        prog.bit_global.assign(plan.is_global.begin(), plan.is_global.end());
+        for (int i = 0; i < s; i++) {
+            if (!plan.is_global[i]) local |= 1ull << (s - 1 - i);
+            ng += plan.is_global[i] != 0;
+        }
+        if (ng != plan.n_global) return "loop program: n_global differs from the global flags";
         if (plan.segs.back().E != 0) return "loop program: the last segment cannot sum local bits";
         if (plan.segs.back().Sum != local) return "loop program: the last segment must follow every local summation";
+        for (const Plan::Seg& g : plan.segs)
+            if (g.E & ~local) return "loop program: a segment sums a global bit";
         prog.s_global = plan.n_global;
     } else {
         prog.s_global = s;
@@ -639,7 +649,9 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     st.bytes = (8.0 + 8.0 + 32.0) * (double)req.M;
     acc(st, F.buf, ((int64_t)F.rows.size() << dF) * 8, false);
     if (segmented) {
-        const uint64_t glob = plan.n_global == 0 ? 0ull : (((1ull << plan.n_global) - 1) << (s - plan.n_global));
+        uint64_t glob = 0;
+        for (int i = 0; i < s; i++)
+            if (plan.is_global[i]) glob |= 1ull << (s - 1 - i);
         if (nat[final_slot] & ~glob) return "loop program: the final tensor still depends on a local bit";
         prog.segs.back().steps.push_back(st);
         // K_INSTANTIATE first in every segment that instantiates sliced leaves

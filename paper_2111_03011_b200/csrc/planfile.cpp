@@ -9,6 +9,7 @@
 //    "order":   [[i, j], ...],                             // leaf slots; result stored at i
 //    "sliced":  [[q, k], ...],                             // sliced wires in loop-bit order (MSB first)
 //    "n_global": g,                                        // -1: flat slicing (all bits are slice ids)
+//    "global":  [1 if sliced[i] is a slice-id bit, ...],
 //    "step_seg": [segment of step p, ...],
 //    "segs":    [[D, Sum, E], ...]}                        // tau-bit masks (decimal)
 #include <cctype>
@@ -132,7 +133,9 @@ std::string save_plan(const Network& net, const std::vector<Leaf>& leaves, const
     f << "],\n \"sliced\": [";
     for (size_t i = 0; i < plan.sliced.size(); i++)
         f << (i ? "," : "") << "[" << net.edges[plan.sliced[i]].q << "," << net.edges[plan.sliced[i]].k << "]";
-    f << "],\n \"n_global\": " << (plan.segs.empty() ? -1 : plan.n_global) << ",\n \"step_seg\": [";
+    f << "],\n \"n_global\": " << (plan.segs.empty() ? -1 : plan.n_global) << ",\n \"global\": [";
+    for (size_t i = 0; i < plan.is_global.size(); i++) f << (i ? "," : "") << (int)plan.is_global[i];
+    f << "],\n \"step_seg\": [";
     for (size_t p = 0; p < plan.step_seg.size(); p++) f << (p ? "," : "") << plan.step_seg[p];
     f << "],\n \"segs\": [";
     for (size_t j = 0; j < plan.segs.size(); j++)
@@ -193,6 +196,14 @@ std::string load_plan(const Network& net, const std::vector<Leaf>& leaves, const
         if (!jss || !jsg || jss->kind != JV::ARR || jsg->kind != JV::ARR) return "plan file: missing segments";
         if (ng > s) return "plan file: n_global > number of sliced wires";
         pl.n_global = ng;
+        const JV* jgl = get("global");
+        if (!jgl || jgl->kind != JV::ARR || (int)jgl->arr.size() != s) return "plan file: missing global flags";
+        int cnt = 0;
+        for (const JV& x : jgl->arr) {
+            pl.is_global.push_back(x.i64() ? 1 : 0);
+            cnt += x.i64() ? 1 : 0;
+        }
+        if (cnt != ng) return "plan file: n_global differs from the global flags";
         for (const JV& x : jsg->arr) {
             if (x.kind != JV::ARR || x.arr.size() != 3) return "plan file: bad segment";
             Plan::Seg g;
@@ -212,13 +223,14 @@ std::string load_plan(const Network& net, const std::vector<Leaf>& leaves, const
             last = j;
             pl.step_seg.push_back(j);
         }
-        // the local bits (below the global ones) must each be summed exactly once
-        uint64_t summed = 0;
+        // the local bits must each be summed exactly once
+        uint64_t summed = 0, local = 0;
+        for (int i = 0; i < s; i++)
+            if (!pl.is_global[i]) local |= 1ull << (s - 1 - i);
         for (const Plan::Seg& g : pl.segs) {
             if (g.E & summed) return "plan file: a local bit is summed twice";
             summed |= g.E;
         }
-        const uint64_t local = (s - ng) >= 64 ? ~0ull : ((1ull << (s - ng)) - 1);
         if (summed != local) return "plan file: the summed bits must be exactly the local bits";
     }
     plan = pl;

@@ -117,6 +117,7 @@ inline StepCost step_cost(int a, int b, int c, int u, double rA, double rB, doub
 
 struct Node {
     int left = -1, right = -1, leaf = -1, parent = -1;
+    int seg = -1;        // loop-program segment of an internal node (-1: none); reconfiguration stays inside one
     Bits legs;           // dense legs of the result (unsliced)
     uint64_t q = 0;      // fixed final qubits
     double rows = 1;
@@ -197,7 +198,7 @@ bool reconf_node(Tree& t, int v, Ctx& cx) {
         double bs = -1;
         for (int i = 0; i < (int)front.size(); i++) {
             const Node& N = t.nodes[front[i]];
-            if (N.leaf >= 0) continue;
+            if (N.leaf >= 0 || N.seg != t.nodes[v].seg) continue;
             double s = node_size(N, cx.sliced);
             if (s > bs) { bs = s; bi = i; }
         }
@@ -295,6 +296,7 @@ bool reconf_node(Tree& t, int v, Ctx& cx) {
         N.left = a;
         N.right = b;
         N.leaf = -1;
+        N.seg = t.nodes[v].seg;
         t.nodes[a].parent = node;
         t.nodes[b].parent = node;
         N.legs = t.nodes[a].legs ^ t.nodes[b].legs;
@@ -923,6 +925,104 @@ Checkpoints checkpoint_dp(const StemEvents& ev, int J, double lambda) {
     return best;
 }
 
+// Loop nest of a checkpointed stem.  Every sliced edge gets the segment interval [a, b] over which it is looped
+// (opened at segment a, summed at the end of segment b; b = J-1: a global slice, summed by the readout).  The
+// intervals are made laminar (nested or disjoint) by extending crossing ones -- the cheaper of "sum the earlier
+// one later" and "open the later one earlier" -- so that the loops form a proper nest: each segment then runs
+// exactly 2^|D_j| times, D_j = the intervals containing j.  Bit significance = preorder of the interval forest
+// (outer loops and earlier sequential loops more significant): with it, no segment re-runs because of a loop
+// it does not depend on, and every summation completes before its consumers run.
+struct LoopNest {
+    std::vector<int> a, b;        // per sliced edge (StemEvents order)
+    std::vector<int> order;       // edge indices, most significant first
+    std::vector<double> segc;     // per segment: modelled CMAC of one run (steps + accumulate pass)
+    double cost = 0;              // sum_j segc[j] * 2^|D_j|
+};
+
+double nest_cost(const std::vector<double>& segc, const std::vector<int>& a, const std::vector<int>& b) {
+    double c = 0;
+    for (int j = 0; j < (int)segc.size(); j++) {
+        int d = 0;
+        for (size_t e = 0; e < a.size(); e++) d += a[e] <= j && j <= b[e];
+        c += segc[j] * std::ldexp(1.0, d);
+    }
+    return c;
+}
+
+LoopNest loop_nest(const StemEvents& ev, const std::vector<int>& cp, int min_global) {
+    const int J = (int)cp.size(), ns = (int)ev.edge.size(), K = (int)ev.c.size();
+    auto seg_of_pos = [&](int pos) {
+        int j = 0;
+        while (cp[j] < pos) j++;
+        return j;
+    };
+    LoopNest L;
+    L.a.resize(ns);
+    L.b.resize(ns);
+    for (int e = 0; e < ns; e++) {
+        L.a[e] = seg_of_pos(std::max(1, ev.ab[e].first));
+        L.b[e] = seg_of_pos(ev.ab[e].second);
+    }
+    std::vector<double> base(J, 0.0);
+    for (int k = 1; k < K; k++) base[seg_of_pos(k)] += ev.c[k];
+    auto costs = [&]() {  // segment costs incl. one accumulate pass where a local loop ends
+        std::vector<double> sc = base;
+        for (int j = 0; j + 1 < J; j++) {
+            bool acc = false;
+            for (int e = 0; e < ns; e++) acc = acc || L.b[e] == j;
+            if (acc) sc[j] += 3 * ev.size[cp[j]];
+        }
+        return sc;
+    };
+    auto laminarize = [&]() {
+        for (int guard = 0; guard < 100000; guard++) {
+            int x = -1, y = -1;
+            for (int i = 0; i < ns && x < 0; i++)
+                for (int k = 0; k < ns; k++)
+                    if (L.a[i] < L.a[k] && L.a[k] <= L.b[i] && L.b[i] < L.b[k]) {
+                        x = i;
+                        y = k;
+                        break;
+                    }
+            if (x < 0) return;
+            const std::vector<double> sc = costs();
+            std::vector<int> b1 = L.b, a2 = L.a;
+            b1[x] = L.b[y];      // sum x later
+            a2[y] = L.a[x];      // open y earlier
+            if (nest_cost(sc, L.a, b1) <= nest_cost(sc, a2, L.b)) L.b = b1;
+            else L.a = a2;
+        }
+    };
+    laminarize();
+    for (;;) {  // at least min_global global slices: promote the cheapest local loops
+        int ng = 0;
+        for (int e = 0; e < ns; e++) ng += L.b[e] == J - 1;
+        if (ng >= std::min(min_global, ns)) break;
+        int be = -1;
+        double bc = 1e308;
+        const std::vector<double> sc = costs();
+        for (int e = 0; e < ns; e++) {
+            if (L.b[e] == J - 1) continue;
+            std::vector<int> b1 = L.b;
+            b1[e] = J - 1;
+            const double c = nest_cost(sc, L.a, b1);
+            if (c < bc) { bc = c; be = e; }
+        }
+        L.b[be] = J - 1;
+        laminarize();
+    }
+    L.segc = costs();
+    L.cost = nest_cost(L.segc, L.a, L.b);
+    // preorder of the laminar forest: start ascending, end descending (parents before children)
+    L.order.resize(ns);
+    for (int e = 0; e < ns; e++) L.order[e] = e;
+    std::stable_sort(L.order.begin(), L.order.end(), [&](int x, int y) {
+        if (L.a[x] != L.a[y]) return L.a[x] < L.a[y];
+        return L.b[x] > L.b[y];
+    });
+    return L;
+}
+
 Tree sweep_tree(const std::vector<Leaf>& leaves, const std::vector<int>& pi, RowModel& rm) {
     const int NL = (int)leaves.size();
     Tree t;
@@ -962,6 +1062,43 @@ std::vector<int> leaf_order(const Tree& t) {
         if (N.leaf >= 0) { out.push_back(N.leaf); continue; }
         st.push_back(N.right);
         st.push_back(N.left);
+    }
+    return out;
+}
+
+// loop programs: (i, j) pairs plus the segment of each step, children visited stem-first (the child whose
+// subtree holds the lowest segment first), so that segments are nondecreasing in program order
+std::vector<std::pair<int, int>> tree_order_seg(const Tree& t, std::vector<int>& step_seg) {
+    std::vector<int> minseg(t.nodes.size(), INT_MAX);
+    std::function<int(int)> ms = [&](int x) -> int {
+        const Node& N = t.nodes[x];
+        if (N.leaf >= 0) return minseg[x] = INT_MAX;
+        return minseg[x] = std::min(N.seg, std::min(ms(N.left), ms(N.right)));
+    };
+    ms(t.root);
+    std::vector<std::pair<int, int>> out;
+    step_seg.clear();
+    std::vector<int> rep(t.nodes.size(), -1);
+    std::vector<std::pair<int, int>> st = {{t.root, 0}};
+    while (!st.empty()) {
+        auto [x, s] = st.back();
+        st.pop_back();
+        const Node& N = t.nodes[x];
+        if (N.leaf >= 0) {
+            rep[x] = N.leaf;
+            continue;
+        }
+        const bool swap = minseg[N.right] < minseg[N.left];
+        const int first = swap ? N.right : N.left, second = swap ? N.left : N.right;
+        if (s == 0) {
+            st.push_back({x, 1});
+            st.push_back({second, 0});
+            st.push_back({first, 0});
+        } else {
+            out.push_back({rep[first], rep[second]});
+            step_seg.push_back(N.seg);
+            rep[x] = rep[first];
+        }
     }
     return out;
 }
@@ -1089,12 +1226,20 @@ std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         if (!ok) continue;
         // leaves larger than the bound cannot be sliced further by this planner
         StemEvents sev = stem_events(S, st, net, slot_of_tensor);
+        // checkpoints: the DP's candidates for every segment count, scored by the laminar loop nest's cost
         Checkpoints c;
-        for (double lambda = 0.0;; lambda = lambda > 0 ? lambda * 4 : 1e-3) {
-            c = checkpoint_dp(sev, std::max(1, opt.max_segments), lambda);
-            if (c.persist <= pbudget || lambda > 1e12) break;
+        c.cost = 1e308;
+        for (int Jc = 1; Jc <= std::max(1, opt.max_segments); Jc++) {
+            Checkpoints cj;
+            for (double lambda = 0.0;; lambda = lambda > 0 ? lambda * 4 : 1e-3) {
+                cj = checkpoint_dp(sev, Jc, lambda);
+                if (cj.persist <= pbudget || lambda > 1e12) break;
+            }
+            if (cj.persist > pbudget) continue;
+            cj.cost = loop_nest(sev, cj.cp, std::max(0, opt.n_sliced)).cost;
+            if (cj.cost < c.cost) c = cj;
         }
-        if (c.persist > pbudget) continue;
+        if (c.cp.empty()) continue;
         if (verbose)
             fprintf(stderr, "[plan] sweep %d: s %zu, %zu segments, cost %.3e, persist 2^%.1f, peak 2^%.1f (%.1f s)\n", k,
                     sev.edge.size(), c.cp.size(), c.cost, std::log2(std::max(1.0, c.persist)), std::log2(peak_of(st)),
@@ -1112,7 +1257,6 @@ std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     // ---------------- 3. the plan: stem order, bits, segments
     Plan pl;
     Tree t = sweep_tree(leaves, best_st.pi, rm);
-    pl.order = tree_order(t);
     const std::vector<int>& cp = best_cp.cp;
     const int J = (int)cp.size();
     auto seg_of_pos = [&](int pos) {
@@ -1120,59 +1264,41 @@ std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         while (cp[j] < pos) j++;
         return j;
     };
-    pl.step_seg.resize(pl.order.size());
-    for (size_t p = 0; p < pl.order.size(); p++) pl.step_seg[p] = seg_of_pos((int)p + 1);
-    // summation segment of each sliced edge: the segment containing its close position; the last segment's
-    // edges are global
-    const int ns = (int)best_ev.edge.size();
-    std::vector<int> sumseg(ns);
-    for (int i = 0; i < ns; i++) sumseg[i] = seg_of_pos(best_ev.ab[i].second);
-    // at least opt.n_sliced global bits (parallel slices): promote the latest-summed local edges
+    for (int k = 1; k < NL; k++) t.nodes[NL + k - 1].seg = seg_of_pos(k);
+    // branch merging inside each segment: subtree reconfiguration under the
+    // roofline-time model turns runs of small absorptions into branches contracted first and absorbed by
+    // one tensor-core-sized step; it never moves work across a checkpoint
+    Bits Sall;
+    for (int e = 0; e < (int)best_sliced.size(); e++)
+        if (best_sliced[e]) Sall.set(e);
+    const double t_before = eval_tree(t, Sall).time;
     {
-        int ng = 0;
-        for (int i = 0; i < ns; i++) ng += sumseg[i] == J - 1;
-        while (ng < opt.n_sliced && ng < ns) {
-            int bi = -1;
-            for (int i = 0; i < ns; i++)
-                if (sumseg[i] < J - 1 && (bi < 0 || sumseg[i] > sumseg[bi])) bi = i;
-            sumseg[bi] = J - 1;
-            ng++;
-        }
+        Ctx cx{&rm, Sall, opt.max_elems};
+        reconfigure(t, cx, elapsed() + std::max(2.0, 0.25 * budget), t0);
     }
-    std::vector<int> idx(ns);
-    for (int i = 0; i < ns; i++) idx[i] = i;
-    // bit order: global first (MSB), then local by summation segment descending (earliest summed = LSB)
-    std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return sumseg[x] > sumseg[y]; });
+    const double t_after = eval_tree(t, Sall).time;
+    pl.order = tree_order_seg(t, pl.step_seg);
+    // loop nest: laminar intervals, at least opt.n_sliced global slices, bit order = interval-forest preorder
+    const int ns = (int)best_ev.edge.size();
+    LoopNest LN = loop_nest(best_ev, cp, std::max(0, opt.n_sliced));
     pl.n_global = 0;
-    for (int i : idx) {
-        pl.sliced.push_back(best_ev.edge[i]);
-        if (sumseg[i] == J - 1) pl.n_global++;
+    for (int r = 0; r < ns; r++) {
+        const int e = LN.order[r];
+        pl.sliced.push_back(best_ev.edge[e]);
+        pl.is_global.push_back(LN.b[e] == J - 1 ? 1 : 0);
+        pl.n_global += LN.b[e] == J - 1;
     }
     auto bit = [&](int rank) { return 1ull << (ns - 1 - rank); };
     pl.segs.resize(J);
     for (int j = 0; j < J; j++) {
-        const int p = j == 0 ? 0 : cp[j - 1], q = cp[j];
         for (int r = 0; r < ns; r++) {
-            const int i = idx[r];
-            const auto& ab = best_ev.ab[i];
-            const int close = sumseg[i] == J - 1 ? NL - 1 : ab.second;  // promoted globals stay open
-            if (ab.first <= q && close > p) pl.segs[j].D |= bit(r);
-            if (sumseg[i] == j && j < J - 1) pl.segs[j].E |= bit(r);
+            const int e = LN.order[r];
+            if (LN.a[e] <= j && j <= LN.b[e]) pl.segs[j].D |= bit(r);
+            if (LN.b[e] == j && j < J - 1) pl.segs[j].E |= bit(r);
+            if (LN.b[e] < j) pl.segs[j].Sum |= bit(r);
         }
-        for (int jj = 0; jj < j; jj++) pl.segs[j].Sum |= pl.segs[jj].E;
     }
-    // modelled cost of the program (promotions included)
-    {
-        double tot = 0;
-        for (int j = 0; j < J; j++) {
-            const int p = j == 0 ? 0 : cp[j - 1], q = cp[j];
-            double c = 0;
-            for (int k = p + 1; k <= q; k++) c += best_ev.c[k];
-            if (pl.segs[j].E) c += 3 * best_ev.size[q];
-            tot += c * std::ldexp(1.0, __builtin_popcountll(pl.segs[j].D));
-        }
-        pl.total_cmac = tot;
-    }
+    pl.total_cmac = LN.cost;
     pl.persist_elems = best_cp.persist;
     TreeEval ev = eval_tree(t, Bits());
     (void)ev;
@@ -1186,7 +1312,17 @@ std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         pl.cmac = c;
         pl.peak = pk;
     }
+    // modelled time over all slices: per segment, the tree's step times of one iteration x its runs
+    {
+        std::vector<double> segt(J, 0.0);
+        for (int x = NL; x < (int)t.nodes.size(); x++)
+            if (t.nodes[x].seg >= 0) segt[t.nodes[x].seg] += node_step(t, x, Sall).time;
+        pl.time_s = 0;
+        for (int j = 0; j < J; j++) pl.time_s += segt[j] * std::ldexp(1.0, __builtin_popcountll(pl.segs[j].D));
+    }
     if (verbose) {
+        fprintf(stderr, "[plan] branch merge: one-iteration model time %.3e -> %.3e s; whole program %.3e s\n", t_before,
+                t_after, pl.time_s);
         fprintf(stderr, "[plan] loop program: %d global + %d local bits, %d segments, total %.3e CMAC, persist 2^%.1f\n",
                 pl.n_global, ns - pl.n_global, J, pl.total_cmac, std::log2(std::max(1.0, pl.persist_elems)));
         for (int j = 0; j < J; j++)

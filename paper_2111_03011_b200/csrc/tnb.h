@@ -101,14 +101,16 @@ struct Plan {
     std::vector<std::pair<int, int>> tied_wire;  // (q, k): the projector's wire, right before the gate
     double cmac = 0, bytes = 0, time_s = 0;  // per slice
     double peak = 0;                         // elements, per slice
-    // Loop program (head/tail local slices; planner.cpp checkpoint_dp).  Empty `segs`: flat
-    // slicing, every sliced edge is a slice-id bit.  Otherwise the first n_global entries of `sliced` are the
-    // slice-id bits (global slices, summed by the readout) and the rest are local loop bits summed inside the
-    // program.  Loop index tau has s = sliced.size() bits, sliced[i] <-> tau bit (s-1-i); tau = (sigma <<
-    // (s - n_global)) | local.  Pairwise step p belongs to segment step_seg[p] (nondecreasing); a segment runs
-    // at tau iff all its Sum bits are 1 and its D bits differ from its previous run; E = local bits summed
-    // (accumulated) at the end of the segment.
+    // Loop program (head/tail local slices; planner.cpp loop_nest).  Empty `segs`: flat
+    // slicing, every sliced edge is a slice-id bit.  Otherwise `sliced` lists every looped edge by loop
+    // significance (outermost first); is_global marks the slice-id bits (global slices, summed by the readout;
+    // slice id sigma's bits are the global entries in list order), the rest are local loop bits summed inside
+    // the program.  Loop index tau has s = sliced.size() bits, sliced[i] <-> tau bit (s-1-i).  Pairwise step p
+    // belongs to segment step_seg[p] (nondecreasing); the executor enumerates tau in increasing order (global
+    // bits restricted to the caller's slice ids) and runs a segment when all its Sum bits are 1 and its D bits
+    // differ from its previous run; E = local bits summed (accumulated) at the end of the segment.
     int n_global = -1;
+    std::vector<char> is_global;   // loop program: per entry of `sliced`, 1 = a slice-id bit (any position)
     std::vector<int> step_seg;
     struct Seg {
         uint64_t D = 0, Sum = 0, E = 0;
@@ -322,7 +324,8 @@ struct Program {
         std::vector<Step> steps;
     };
     std::vector<Seg> segs;
-    int s_global = 0;          // slice-id bits (the top bits of the loop index)
+    int s_global = 0;          // slice-id bits
+    std::vector<char> bit_global;  // per sliced index (MSB first): 1 = slice-id bit
     int64_t lvl_bytes = 0;     // REG_LVL: tensors kept across loop iterations (checkpoints, accumulators)
     double total_cmac = 0;     // over all 2^s_global slices, counting each segment's runs
     // plan dump support
