@@ -10,6 +10,8 @@ Contents
   tn_brute.py    brute-force enumeration of the tensor network for tiny circuits (O6)
   rows.py        sparse-state row tables and parent maps (O7)
   metrics.py     F_exact, F_norm, F_sparse, linear XEB, within-group sampler (O5, a9)
+  tn_einsum.py   closed-network contraction of single amplitudes (numpy tensordot, own greedy order),
+                 for the 53-qubit spot checks (SURVEY §8(c) "53q amplitudes")
 
 Parity status (DESIGN.md §Oracle pins): every function above is pinned by a
 `-m "not gpu"` test against a closed form, a printed paper example, an invariant, a

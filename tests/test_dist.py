@@ -139,7 +139,7 @@ def test_contract_distributed_two_ranks_on_one_gpu(tmp_path, oracle_built, metho
     n = circ["n"]
     bits = c.bitstrings(n)
     ss = T.SparseState(circ, bits, c.open_mask(n))
-    ss.plan(1 << 12, n_sliced=3, method=method, time_budget_s=3.0)
+    ss.plan(1 << 12, n_sliced=(-1 if method == 1 else 3), method=method, time_budget_s=3.0)
     p = str(tmp_path / "plan.json")
     ss.save_plan(p)
     ctx = mp.get_context("spawn")

@@ -1,0 +1,71 @@
+"""53-qubit Sycamore layout (the north-star size) through loop programs on the GPU.  The 2^53 state vector is out
+of reach, so parity rests on the checks SURVEY §8(c) names for 53q ("53q amplitudes"):
+  * a few amplitudes of ONE global slice recomputed on the CPU by an independent closed-network contraction
+    (oracle/tn_einsum.py: numpy tensordot, its own greedy order; Pi_v on the slice's global wires, the local
+    wires summed as in the product);
+  * the sum over ALL slices is the exact state, so F_norm = (2^n/M) sum |a|^2 ~= 1 for
+    uniformly drawn fixed parts, and the amplitudes follow Porter-Thomas at depth.
+Inputs: the config-4 layout and open qubits (tn_inputs/configs.py), seeded requests."""
+import numpy as np
+import pytest
+
+from tn_inputs import bitstrings as bs
+from tn_inputs import circuits as cc
+from tn_inputs import configs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_2111_03011_b200 as T
+    T.lib()
+    return T
+
+
+def syc53(m, L, seed=1004):
+    c = configs.get(4)
+    circ = cc.generate_circuit(c.qubits(), m, "ABCDCDAB", seed)
+    n = circ["n"]
+    oq = c.open_ids(n)
+    bits = bs.generate_groups(n, oq, L, 2004)
+    return circ, n, bits, bs.qubit_mask(n, oq)
+
+
+def test_53q_m6_slice_amplitudes_match_closed_network(T):
+    """53q m=6, 1024 groups x 64, loop program at max_tensor_size 2^18 (global and local slices): amplitudes of
+    one global slice vs oracle/tn_einsum for 6 requested bitstrings."""
+    from oracle import tn_einsum
+    from tests.helpers import rel_l2
+    circ, n, bits, om = syc53(6, 1024)
+    ss = T.SparseState(circ, bits, om)
+    info = ss.plan(1 << 18, n_sliced=3, method=2, max_segments=6, time_budget_s=10.0)
+    assert info["s"] >= 3 and info["s_local"] >= 1, info
+    ss.bind(0, pipelines=2)
+    s = info["s"]
+    sigma = 5 % (1 << s)
+    amps = ss.contract([sigma]).cpu().numpy().astype(complex)
+    vals = [(sigma >> (s - 1 - i)) & 1 for i in range(s)]
+    fixed = {tuple(w): v for w, v in zip(info["sliced_wires"], vals)}
+    js = [0, 1, 63, 4097, 30000, len(bits) - 1]
+    want = np.array([tn_einsum.amplitude(circ, int(bits[j]), fixed) for j in js])
+    got = amps[js]
+    assert rel_l2(got, want) < 1e-4, (got, want)
+
+
+def test_53q_m8_all_slices_norm_and_porter_thomas(T):
+    """53q m=8 with the config-4 request (2^14 groups x 64 = 2^20 amplitudes), loop program at 2^28: the sum
+    over every global slice has F_norm = 1 within the sampling error of 2^20 amplitudes, and 2^n |a|^2 is
+    close to Exp(1)."""
+    from oracle import metrics
+    circ, n, bits, om = syc53(8, 1 << 14)
+    ss = T.SparseState(circ, bits, om)
+    info = ss.plan(1 << 28, n_sliced=3, method=2, max_segments=6, time_budget_s=20.0)
+    ss.bind(0, pipelines=1)
+    amps = ss.contract(range(1 << info["s"])).cpu().numpy().astype(complex)
+    fn = metrics.f_norm(amps, n)
+    assert abs(fn - 1.0) < 0.02, fn
+    ks = metrics.porter_thomas_ks((2.0 ** n) * np.abs(amps) ** 2)
+    assert ks < 0.05, ks

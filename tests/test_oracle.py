@@ -586,3 +586,20 @@ def test_companion_fidelity_factor(oracle_built):
             Fs[th].append(metrics.f_exact(psi, approx))
     assert min(Fs[math.pi / 2]) > 1 - 1e-12
     assert abs(np.mean(Fs[math.pi / 3]) - 0.875) < 0.06, Fs[math.pi / 3]
+
+
+@pytest.mark.parametrize("seed", [5, 9])
+def test_closed_network_matches_statevector(oracle_built, seed):
+    """oracle/tn_einsum (closed-network contraction, numpy tensordot) = the state-vector oracle with the same
+    projectors inserted (12 qubits, 6 cycles, three sliced wires), for several bitstrings."""
+    from oracle import sv, tn_einsum
+    circ = cc.generate_circuit(cc.rect_layout(3, 4), 6, "ABCDCDAB", seed)
+    x = np.array([5, 1234, 4095, 77, 2048], np.uint64)
+    wires = [(1, 3, 1), (5, 4, 0), (7, 5, 1)]
+    want, _ = sv.amplitudes(circ, x, wires)
+    got = np.array([tn_einsum.amplitude(circ, int(v), {(q, k): b for q, k, b in wires}) for v in x])
+    assert np.abs(got - want).max() < 1e-14
+    # and without projectors (the unsliced amplitude)
+    want0, _ = sv.amplitudes(circ, x)
+    got0 = np.array([tn_einsum.amplitude(circ, int(v)) for v in x])
+    assert np.abs(got0 - want0).max() < 1e-14
