@@ -3,11 +3,14 @@
 
     python bench.py [--gpus N --steps K --warmup W --config C --impl {ours,reference}]
 
-A step = one tn_contract over the workload's whole slice set S (slice
-instantiate, pairwise contractions, readout+accumulate) plus, for N > 1, the NCCL all-reduce of the M
-amplitudes.  S is split into N contiguous blocks (strong scaling: the total work is fixed).
-Metric (BASELINE.json): slices/s (aggregate over ranks) with complex TFLOP/s (8 x CMAC/s) and
-the roofline fraction of the dominant kernel alongside.
+Workload (BASELINE.json north_star / metric): config 4 = 53-qubit Sycamore layout, m=14, M = 2^20 requested
+amplitudes (2^14 groups x 64), contracted by the loop program in plans/config4.json (global slices = the
+slice ids of tn_contract; local slices are summed inside each one, the head is reused across slices,
+P:L89-L91).  A full run is 2^s global slices; one step contracts a bounded block of them
+(`--block` per GPU, weak scaling: every rank its own block) plus the NCCL all-reduce of the M amplitudes,
+and the time to all 2^20 amplitudes (the whole slice set) is extrapolated from the measured steps and the
+loop program's segment run counts (labelled as such).  Config 3 (30 qubits, all 2^8 slices per step) is
+measured as a secondary line at N=1.
 
 Rank 0 prints ONE JSON line.  Multi-GPU: launched by torch.distributed.run (one rank per GPU, NCCL).
 """
@@ -32,6 +35,8 @@ os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 from tn_inputs import configs  # noqa: E402
 
 METRIC = "slices/sec & complex TFLOP/s (frac of peak) at 1/2/4/8 B200; time to 1e6 amplitudes"
+DEFAULT_BLOCK = {4: 4, 3: 256}       # global slices per rank per step
+DEFAULT_PIPES = {4: 1, 3: 16}
 
 
 def peaks():
@@ -41,6 +46,15 @@ def peaks():
         return {"hbm_gbs": d["hbm_gbs"], "bf16": d["bf16_tflops"], "bf16_sust": d["bf16_tflops_sustained"],
                 "src": "measured (MEASURED_PEAKS.json)"}
     return {"hbm_gbs": 6650.0, "bf16": 1590.0, "bf16_sust": 1400.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+def refuse_diagnostic_build():
+    """A library built with diagnostics flags (e.g. -DTNB_DIAG_SKIP, which can drop launches) is never
+    benchmarked."""
+    stamp = os.path.join(ROOT, "paper_2111_03011_b200", "_build", "executor.cu.o.flags")
+    if os.path.exists(stamp) and open(stamp).read().strip():
+        raise SystemExit(f"bench.py: libtnb200.so was built with TNB_NVCC_FLAGS={open(stamp).read().strip()!r}; "
+                         "rebuild without diagnostics flags")
 
 
 # ------------------------------------------------------------------------------ clocks sampler
@@ -89,49 +103,65 @@ class Clocks:
 
 # ------------------------------------------------------------------------------ oracle (CPU baseline)
 
-def oracle_sample(cfg, max_seconds: float = 20.0):
-    """Time the oracle (oracle/sv.c, fp64 state vector, OpenMP over all host cores) on a bounded sample of
-    one slice of the workload: the first G gate passes of the projector-inserted state-vector run of
-    slice 0, with G grown until ~max_seconds of CPU work; extrapolated linearly to the whole circuit
-    (one slice = one full run over all gates)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_sample(cfg, threads: int, max_seconds: float = 20.0):
+    """Time the oracle (oracle/sv.c: fp64 state vector) on a bounded sample of the step's output.  A step sums
+    ALL slices, and the oracle gets that sum in ONE state-vector run of the circuit (Sigma_v Pi_v = I on every
+    sliced wire), so one step = one full run over all G gates.  Sample: the first `take`
+    gate passes (grown until ~max_seconds / 3), extrapolated linearly to G."""
     from oracle import sv  # test infrastructure: allowed only in this leg
     from tn_inputs import circuits as cc
     circ = cfg.circuit()
     gates = cc.gate_list(circ)
     G = len(gates)
-    cores = os.cpu_count() or 1
     take = 4
-    t_used = 0.0
     while True:
         sub = dict(circ)
         sub["moments"] = [gates[:take]]
         t0 = time.perf_counter()
-        sv.amplitudes(sub, np.zeros(1, np.uint64), threads=cores)
+        sv.amplitudes(sub, np.zeros(1, np.uint64), threads=threads)
         t_used = time.perf_counter() - t0
         if t_used > max_seconds / 3 or take >= G:
             break
         take = min(G, take * 4)
-    # subtract nothing: state allocation + |0> init are part of the oracle run as it stands
-    per_slice = t_used * G / take
-    return {"kind": "oracle", "cores": cores, "value": 1.0 / per_slice, "unit": "slices/s",
-            "sample": f"first {take} of {G} gate passes of one {circ['n']}-qubit slice (fp64 state vector, "
-                      f"{cores} OpenMP threads), {t_used:.1f} s, extrapolated linearly to {per_slice:.1f} s/slice"}
+    per_step = t_used * G / take
+    return {"kind": "oracle", "cores": threads, "value": 1.0 / per_step, "unit": "steps/s",
+            "seconds_per_step": per_step,
+            "sample": f"first {take} of {G} gate passes of the {circ['n']}-qubit fp64 state vector (one run = the "
+                      f"all-slices sum), {threads} OpenMP thread(s), {t_used:.1f} s, extrapolated linearly to "
+                      f"{per_step:.1f} s per step; CPU {cpu_model()}"}
 
 
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
+    if cfg.cfg >= 4:
+        print(json.dumps({"impl": "reference", "unavailable": "the oracle is a fp64 state vector: 2^53 amplitudes "
+                          "(128 PiB) for the 53-qubit workload; bench.py --impl reference --config 3 times it on "
+                          "the 30-qubit config"}), flush=True)
+        return
+    cores = os.cpu_count() or 1
     steps = []
     for _ in range(args.warmup):
-        oracle_sample(cfg, max_seconds=args.ref_seconds)
+        oracle_sample(cfg, cores, max_seconds=args.ref_seconds)
     for _ in range(args.steps):
-        steps.append(oracle_sample(cfg, max_seconds=args.ref_seconds))
-    v = statistics.median(s["value"] for s in steps)
+        steps.append(oracle_sample(cfg, cores, max_seconds=args.ref_seconds))
+    nS = 1 << cfg.n_sliced
+    v = statistics.median(nS * s["value"] for s in steps)  # slices/s: a step is all 2^s slices
     s0 = steps[-1]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "slices/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * nS / v, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(cfg),
+            "config": workload_config(cfg, nS),
             "cpu_baseline": {"kind": "oracle", "cores": s0["cores"], "value": v, "unit": "slices/s",
                              "sample": s0["sample"]},
             "e2e": {"value": v, "unit": "slices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -140,81 +170,110 @@ def run_reference(args, cfg, rank, world):
 
 # ------------------------------------------------------------------------------ our arm
 
-def workload_config(cfg) -> dict:
-    """The workload keys both arms report (the GPU arm adds its run-specific keys)."""
+def workload_config(cfg, slices_per_step) -> dict:
+    """The workload keys both arms report."""
     n = cfg.circuit()["n"]
     M = cfg.L << len(cfg.open_ids(n))
-    s = cfg.n_sliced
-    return {"workload": f"config{cfg.cfg}: {cfg.name} ({cfg.layout}, m={cfg.cycles}, M={M}, 2^{s} slices all summed)",
+    return {"workload": f"config{cfg.cfg}: {cfg.name} ({cfg.layout}, m={cfg.cycles}, M={M} = {cfg.L} groups x "
+                        f"{1 << len(cfg.open_ids(n))})",
             "n_qubits": n, "cycles": cfg.cycles, "M": M, "L": cfg.L, "l": 1 << len(cfg.open_ids(n)),
-            "slices": 1 << s, "max_tensor_size": 1 << cfg.log2_tmax}
+            "slices_per_step": slices_per_step, "max_tensor_size": 1 << cfg.log2_tmax}
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-seconds", type=float, default=20.0)
-    ap.add_argument("--trials", type=int, default=0)
-    ap.add_argument("--pipelines", type=int, default=16)
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg = configs.get(args.config)
-
-    if args.impl == "reference":
-        run_reference(args, cfg, rank, world)
-        return
-
-    import torch
-    import torch.distributed as dist
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-
-    import paper_2111_03011_b200 as T
-
-    # ------------------------------------------------------------ setup (not timed): build, plan, bind
-    t0 = time.perf_counter()
+def plan_ss(T, cfg, plan_path, log2_tmax):
     circ = cfg.circuit()
     n = circ["n"]
     bits = cfg.bitstrings(n)
+    t0 = time.perf_counter()
     ss = T.SparseState(circ, bits, cfg.open_mask(n))
     t_build = time.perf_counter() - t0
     t0 = time.perf_counter()
-    pk = cfg.plan_kwargs()
-    if args.trials:
-        pk["trials"] = args.trials
-    info = ss.plan(1 << cfg.log2_tmax, **pk)
-    t_plan = time.perf_counter() - t0
-    if world > 1:  # every rank must contract the same sliced network: compare plan fingerprints
-        fp = torch.tensor([float(hash(tuple(info["sliced_wires"])) % (1 << 52)), info["cmac_per_slice"]],
-                          dtype=torch.float64, device=dev)
-        allfp = [torch.zeros_like(fp) for _ in range(world)]
-        dist.all_gather(allfp, fp)
-        if any(not torch.equal(allfp[0], x) for x in allfp):
-            raise RuntimeError("ranks produced different plans; refusing to sum inconsistent slices")
+    if plan_path and os.path.exists(plan_path):
+        info = ss.plan(1 << log2_tmax, plan_path=plan_path)
+        src = os.path.relpath(plan_path, ROOT)
+    else:
+        info = ss.plan(1 << log2_tmax, **cfg.plan_kwargs())
+        src = "searched"
+    return ss, info, {"build": t_build, "plan": time.perf_counter() - t0, "plan_source": src}
+
+
+def seg_dims(ss, info):
+    """popcount(D_j) of every loop-program segment (from the plan file the ctx would save)."""
+    if info["n_segments"] <= 1 and info["s_local"] == 0:
+        return None
+    import tempfile
+    with tempfile.NamedTemporaryFile(suffix=".json", delete=False) as f:
+        p = f.name
+    ss.save_plan(p)
+    d = json.load(open(p))
+    os.unlink(p)
+    return [bin(int(D)).count("1") for D, _, _ in d["segs"]]
+
+
+def roofline(kind, d, pk, traffic):
+    if kind == "gemm_tcgen05":
+        # 3xTF32 tensor-core GEMM: 3 real GEMMs [Mp x 2K] x [2K x 2N] = 24 flops per complex MAC; peak = TF32
+        # dense = measured bf16 x nominal tf32/bf16 ratio (1.1/2.25)
+        achieved = 24.0 * d["cmac"] / (d["ms"] * 1e-3) / 1e12
+        peak = pk["bf16"] * (1.1 / 2.25)
+        r = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+             "traffic": None, "kernel": "k_gemm_tf32x3", "peak_src": pk["src"] + " bf16 x 1.1/2.25 (tf32)",
+             "useful_complex_tflops": 8.0 * d["cmac"] / (d["ms"] * 1e-3) / 1e12}
+    else:
+        # SIMT / data-movement kernels: bound by HBM or by FP32 FMA issue, whichever roofline time is longer.
+        # FP32 peak for register-operand FFMA (DESIGN.md §6): 148 SMs x 4 SMSPs x 32 lanes / 2 cycles x 2 flop x
+        # 1.965 GHz = 37.2 TFLOP/s; 8 flop per complex MAC
+        alu_peak = 148 * 4 * 32 / 2 * 2 * 1.965e9 / 1e12
+        bw = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+        fl = 8.0 * d["cmac"] / (d["ms"] * 1e-3) / 1e12
+        if 8.0 * d["cmac"] / (alu_peak * 1e12) > d["bytes"] / (pk["hbm_gbs"] * 1e9):
+            r = {"bound": "alu", "achieved": fl, "peak": alu_peak, "unit": "TFLOP/s", "frac": fl / alu_peak,
+                 "traffic": None, "kernel": kind,
+                 "peak_src": "derived: 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz / 2 (FFMA reciprocal "
+                             "throughput 2 cycles per SMSP, B300_MICROARCH.md)", "hbm_frac": bw / pk["hbm_gbs"]}
+        else:
+            r = {"bound": "hbm", "achieved": bw, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": bw / pk["hbm_gbs"],
+                 "traffic": None, "kernel": kind, "peak_src": pk["src"], "alu_frac": fl / alu_peak}
+    r["launches_in_profile"] = d["launches"]
+    r["algorithmic_bytes_per_launch"] = d["bytes"] / max(1, d["launches"])
+    r["avg_launch_ms"] = d["ms"] / max(1, d["launches"])
+    for entry in traffic:
+        if entry.get("kernel") == r["kernel"] and entry.get("config") == d.get("config"):
+            r["traffic"] = entry["dram_bytes_per_launch"]
+            r["traffic_src"] = entry["source"]
+    return r
+
+
+def measure(args, T, torch, dist, dev, stream, cfg, rank, world, flush):
+    """Setup + warm-up + timed steps + e2e + profile of one config; returns a dict (rank 0) for the line."""
+    plan_path = args.plan if (args.plan and cfg.cfg == args.config) else os.path.join(ROOT, "plans",
+                                                                                       f"config{cfg.cfg}.json")
+    ss, info, setup = plan_ss(T, cfg, plan_path, cfg.log2_tmax)
+    if world > 1:
+        from paper_2111_03011_b200.dist import check_same_plan
+        check_same_plan(info)
     t0 = time.perf_counter()
-    stream = torch.cuda.current_stream(dev)
-    ss.bind(local, stream=stream, pipelines=args.pipelines)
+    pipes = args.pipelines or DEFAULT_PIPES.get(cfg.cfg, 8)
+    ss.bind(dev.index, stream=stream, pipelines=pipes)
     torch.cuda.synchronize()
-    t_bind = time.perf_counter() - t0
+    setup["bind"] = time.perf_counter() - t0
     s = info["s"]
     nS = 1 << s
-    from paper_2111_03011_b200.dist import partition
-    block = partition(range(nS), world, rank)
+    loop = info["s_local"] > 0 or info["n_segments"] > 1
+    if cfg.cfg >= 4:
+        # weak scaling over global slices: rank r contracts its own block of B consecutive slices per step
+        B = min(args.block or DEFAULT_BLOCK[4], nS // world)
+        block = list(range(rank * B, (rank + 1) * B))
+        scaling = "weak"
+        per_step_slices = B * world
+    else:
+        from paper_2111_03011_b200.dist import partition
+        block = partition(range(nS), world, rank)
+        B = len(block)
+        scaling = "strong"
+        per_step_slices = nS
     M = ss.M
-
     out = torch.empty(M, dtype=torch.complex64, device=dev)
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
     def step(dst):
         if block:
@@ -227,9 +286,7 @@ def main():
     for _ in range(args.warmup):
         step(out)
     torch.cuda.synchronize()
-
-    # ------------------------------------------------------------ device-timed steps
-    clk = Clocks(local)
+    clk = Clocks(dev.index)
     clk.start()
     total_ms = 0.0
     for _ in range(args.steps):
@@ -248,23 +305,13 @@ def main():
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    slices_per_s = nS / (ms_per_step * 1e-3)
+    ms_per_step = float(t.item()) / args.steps
+    value = per_step_slices / (ms_per_step * 1e-3)
 
-    def spin_sync():
-        """Wait for the device by polling an event (blocking waits on this KVM host wake up late)."""
-        ev = torch.cuda.Event()
-        ev.record(stream)
-        while not ev.query():
-            pass
-
-    # ------------------------------------------------------------ end to end through the public API
-    # host -> device: the step's slice ids from pinned host memory (inside tn_contract); device -> host:
-    # the M amplitudes (pinned); plus the all-reduce for N > 1.
-    ids_pinned = torch.tensor(block if block else [0], dtype=torch.int64).pin_memory()
-    host_out = torch.empty(M, dtype=torch.complex64).pin_memory()
-    e2e_ms = 0.0
+    # end to end through the C ABI's host-buffer path: tn_contract(out_on_device = 0) copies the slice ids in
+    # and the M amplitudes out inside the call; ranks then sum on the host (gloo)
+    hgroup = dist.new_group(backend="gloo") if world > 1 else None
+    host_out = np.empty(M, dtype=np.complex64)
     e2e_each = []
     for _ in range(args.steps):
         flush.zero_()
@@ -272,108 +319,186 @@ def main():
         if world > 1:
             dist.barrier()
         w0 = time.perf_counter()
-        ids = ids_pinned.numpy().astype(np.uint64) if block else []
         if block:
-            ss.contract(ids, out=out)
+            ss.contract_host(block, out=host_out)
         else:
-            out.zero_()
+            host_out[:] = 0
         if world > 1:
-            dist.all_reduce(torch.view_as_real(out), op=dist.ReduceOp.SUM)
-        host_out.copy_(out, non_blocking=True)
-        spin_sync()
+            ht = torch.from_numpy(host_out.view(np.float32))
+            dist.all_reduce(ht, op=dist.ReduceOp.SUM, group=hgroup)
         e2e_each.append((time.perf_counter() - w0) * 1e3)
-        e2e_ms += e2e_each[-1]
-    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([sum(e2e_each)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item()) / args.steps
 
-    # ------------------------------------------------------------ per-launch profile (live, CUDA events)
+    # per-launch profile (one pass through every segment, CUDA events), weighted by each segment's runs in a step
     prof = ss.profile_slice(block[0] if block else 0)
-    launches_per_slice = len(prof)
+    runs = ss.segment_runs(block) if (loop and block) else [len(block)]
     by_kind = {}
+    seg_ms = {}
     for p in prof:
-        k = p["kind"]
-        d = by_kind.setdefault(k, {"ms": 0.0, "launches": 0, "bytes": 0.0, "cmac": 0.0})
+        w = runs[p["seg"]] if (loop and p["seg"] >= 0) else max(1, len(block))
+        d = by_kind.setdefault(p["kind"], {"ms": 0.0, "launches": 0, "bytes": 0.0, "cmac": 0.0, "w_ms": 0.0,
+                                           "config": cfg.cfg})
         d["ms"] += p["ms"]
         d["launches"] += 1
         d["bytes"] += p["bytes"]
         d["cmac"] += p["cmac"]
-    slice_ms = sum(p["ms"] for p in prof)
-    dom = max(by_kind.items(), key=lambda kv: kv[1]["ms"])
+        d["w_ms"] += p["ms"] * w
+        seg_ms[p["seg"]] = seg_ms.get(p["seg"], 0.0) + p["ms"]
+    w_total = sum(d["w_ms"] for d in by_kind.values())
+    dom = max(by_kind.items(), key=lambda kv: kv[1]["w_ms"])
     pk = peaks()
-    tp = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(tp)) if os.path.exists(tp) else []
-    traffic = traffic if isinstance(traffic, list) else [traffic]
-
-    def roofline(kind, d):
-        if kind == "gemm_tcgen05":
-            # algorithmic work of the 3xTF32 tensor-core GEMM: 3 real GEMMs [Mp x 2K] x [2K x 2N] = 24 flops
-            # per complex MAC; peak = TF32 dense = measured bf16 x nominal tf32/bf16 ratio (1.1/2.25)
-            achieved = 24.0 * d["cmac"] / (d["ms"] * 1e-3) / 1e12
-            peak = pk["bf16"] * (1.1 / 2.25)
-            r = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                 "traffic": None, "kernel": "k_gemm_tf32x3", "peak_src": pk["src"] + " bf16 x 1.1/2.25 (tf32)",
-                 "useful_complex_tflops": 8.0 * d["cmac"] / (d["ms"] * 1e-3) / 1e12}
-        else:
-            # SIMT kernels: bound by HBM or by FP32 FMA issue, whichever roofline time is longer.  FP32 peak
-            # for register-operand FFMA: 148 SMs x 4 SMSPs x 32 lanes / 2 cycles (reciprocal
-            # throughput 2, B300_MICROARCH.md) x 2 flop x 1.965 GHz = 37.2 TFLOP/s; 8 flop per complex MAC
-            alu_peak = 148 * 4 * 32 / 2 * 2 * 1.965e9 / 1e12
-            bw = d["bytes"] / (d["ms"] * 1e-3) / 1e9
-            fl = 8.0 * d["cmac"] / (d["ms"] * 1e-3) / 1e12
-            if 8.0 * d["cmac"] / (alu_peak * 1e12) > d["bytes"] / (pk["hbm_gbs"] * 1e9):
-                r = {"bound": "alu", "achieved": fl, "peak": alu_peak, "unit": "TFLOP/s", "frac": fl / alu_peak,
-                     "traffic": None, "kernel": kind,
-                     "peak_src": "derived: 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz / 2 (FFMA reciprocal "
-                                 "throughput 2 cycles per SMSP, B300_MICROARCH.md)",
-                     "hbm_frac": bw / pk["hbm_gbs"]}
-            else:
-                r = {"bound": "hbm", "achieved": bw, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": bw / pk["hbm_gbs"],
-                     "traffic": None, "kernel": kind, "peak_src": pk["src"], "alu_frac": fl / alu_peak}
-        r["share_of_slice"] = d["ms"] / slice_ms
-        r["launches_per_slice"] = d["launches"]
-        r["algorithmic_bytes_per_launch"] = d["bytes"] / max(1, d["launches"])
-        # traffic: DRAM bytes per launch of this kernel from the committed ncu capture (one slice)
-        for entry in traffic:
-            if entry.get("kernel") == r["kernel"]:
-                r["traffic"] = entry["dram_bytes_per_launch"]
-                r["traffic_src"] = entry["source"]
-        return r
-
-    roof = roofline(dom[0], dom[1])
-    roof_tensor = roofline("gemm_tcgen05", by_kind["gemm_tcgen05"]) if (
-        dom[0] != "gemm_tcgen05" and "gemm_tcgen05" in by_kind) else None
+    roof = roofline(dom[0], dom[1], pk, traffic)
+    roof["share_of_step_serialized"] = dom[1]["w_ms"] / w_total
+    roof_tensor = None
+    if dom[0] != "gemm_tcgen05" and "gemm_tcgen05" in by_kind:
+        roof_tensor = roofline("gemm_tcgen05", by_kind["gemm_tcgen05"], pk, traffic)
+        roof_tensor["share_of_step_serialized"] = by_kind["gemm_tcgen05"]["w_ms"] / w_total
+    # CMAC actually executed per step (segment runs x segment CMAC) -> complex TFLOP/s
+    if loop:
+        seg_cmac = {}
+        for p in prof:
+            seg_cmac[p["seg"]] = seg_cmac.get(p["seg"], 0.0) + p["cmac"]
+        cmac_step = world * sum(seg_cmac.get(j, 0.0) * r for j, r in enumerate(runs))
+    else:
+        cmac_step = info["cmac_per_slice"] * per_step_slices
+    # whole-program extrapolation (all 2^s global slices): segment j runs 2^|D_j| times in the laminar loop nest;
+    # per-run times from the profile, calibrated by the measured step (concurrency, launch gaps)
+    extrap = None
+    dims = seg_dims(ss, info) if loop else None
+    if dims is not None:
+        pred_step = sum(seg_ms.get(j, 0.0) * r for j, r in enumerate(runs))
+        scale = ms_per_step / pred_step if pred_step > 0 else 1.0
+        full_ms = sum(seg_ms.get(j, 0.0) * (2.0 ** dims[j]) for j in range(len(dims)))
+        extrap = {"global_slices": nS, "model_s_one_gpu": full_ms * 1e-3, "calibration": scale,
+                  "seconds": full_ms * 1e-3 * scale / world, "n_gpus": world,
+                  "note": "extrapolated, not measured: sum over segments of (profiled time per run) x 2^|D_j| runs, "
+                          "x the measured/profiled step-time ratio, / n_gpus"}
+    else:
+        extrap = {"global_slices": nS, "seconds": ms_per_step * 1e-3 * nS / per_step_slices, "n_gpus": world,
+                  "note": "measured" if per_step_slices == nS else "extrapolated linearly in slices"}
     per_slice_launches, per_contract_launches = ss.launch_counts()
+    launches = args.steps * (sum(runs) if loop else len(block) * per_slice_launches)
+    res = {
+        "ss": ss, "info": info, "value": value, "ms_per_step": ms_per_step, "scaling": scaling,
+        "per_step_slices": per_step_slices, "block": B, "clocks": clocks, "setup": setup,
+        "e2e": {"value": per_step_slices / (e2e_ms * 1e-3), "unit": "slices/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": 8 * len(block) * world, "d2h_bytes_per_step": 8 * M * world,
+                "path": "tn_contract(out_on_device=0) + host all-reduce (gloo) for N > 1",
+                "ms_each": [round(x, 2) for x in e2e_each]},
+        "roofline": roof, "roofline_tensor": roof_tensor, "complex_tflops": 8.0 * cmac_step / (ms_per_step * 1e-3) / 1e12,
+        "cmac_per_step": cmac_step, "extrap": extrap, "pipes": pipes,
+        "kernel_share": {k: round(v["w_ms"] / w_total, 4) for k, v in by_kind.items()},
+        "segment_runs_per_step": runs if loop else None,
+        "gpu_launches": int(launches),
+    }
+    return res
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_sample(cfg)
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=20.0)
+    ap.add_argument("--block", type=int, default=0)
+    ap.add_argument("--pipelines", type=int, default=0)
+    ap.add_argument("--plan", default="")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = configs.get(args.config)
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    refuse_diagnostic_build()
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2111_03011_b200 as T
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    main_r = measure(args, T, torch, dist, dev, stream, cfg, rank, world, flush)
+    info = main_r["info"]
+    main_r["ss"].close()
+    del main_r["ss"]
+    torch.cuda.empty_cache()
+
+    secondary = None
+    if world == 1 and not args.no_secondary and args.config != 3:
+        c3 = configs.get(3)
+        r3 = measure(args, T, torch, dist, dev, stream, c3, rank, world, flush)
+        r3["ss"].close()
+        del r3["ss"]
+        secondary = {"config": workload_config(c3, r3["per_step_slices"]), "value": r3["value"], "unit": "slices/s",
+                     "ms_per_step": r3["ms_per_step"], "complex_tflops": r3["complex_tflops"], "e2e": r3["e2e"],
+                     "roofline": r3["roofline"], "roofline_tensor": r3["roofline_tensor"],
+                     "kernel_share": r3["kernel_share"], "clocks": r3["clocks"], "setup_s": r3["setup"],
+                     "pipelines": r3["pipes"], "gpu_launches": r3["gpu_launches"]}
+        if rank == 0 and not args.no_cpu_baseline:
+            cores = os.cpu_count() or 1
+            one = oracle_sample(c3, 1, max_seconds=10.0)
+            allc = oracle_sample(c3, cores, max_seconds=10.0)
+            nS3 = r3["per_step_slices"]
+            secondary["cpu_baseline"] = {
+                "kind": "oracle", "unit": "slices/s", "value": nS3 / allc["seconds_per_step"], "cores": cores,
+                "value_1core": nS3 / one["seconds_per_step"], "sample": allc["sample"],
+                "sample_1core": one["sample"]}
+            secondary["vs_cpu_baseline"] = r3["value"] / secondary["cpu_baseline"]["value"]
 
     if rank == 0:
-        cmac_total = info["cmac_per_slice"] * nS
+        n = cfg.circuit()["n"]
+        cpu = {"kind": "oracle", "value": None, "unit": "slices/s", "cores": os.cpu_count() or 1,
+               "sample": f"N/A: the oracle is a fp64 state vector of 2^{n} amplitudes; the 30-qubit config's oracle "
+                         "timing is in secondary.cpu_baseline"} if cfg.cfg >= 4 else None
+        if cfg.cfg < 4 and not args.no_cpu_baseline and world == 1:
+            cores = os.cpu_count() or 1
+            allc = oracle_sample(cfg, cores, max_seconds=10.0)
+            cpu = {"kind": "oracle", "unit": "slices/s", "value": main_r["per_step_slices"] / allc["seconds_per_step"],
+                   "cores": cores, "sample": allc["sample"]}
         line = {
-            "metric": METRIC, "value": slices_per_s, "unit": "slices/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "c64", "data": "synthetic",
-            "config": {**workload_config(cfg), "parallelism": f"slices/{world}",
-                       "l2": "flushed (512 MB write) before every timed step; per-slice working set "
-                             f"{info['workspace_bytes'] / 2**30:.2f} GiB > L2",
-                       "setup_s": {"build": t_build, "plan": t_plan, "bind": t_bind}},
-            "complex_tflops": 8.0 * cmac_total / (ms_per_step * 1e-3) / 1e12,
-            "cmac_per_slice": info["cmac_per_slice"], "gemm_cmac_frac": info["gemm_cmac_per_slice"] / max(
-                1.0, info["cmac_per_slice"]),
-            "bytes_per_slice": info["bytes_per_slice"],
-            "time_to_M_amplitudes_s": ms_per_step * 1e-3,
-            "e2e": {"value": nS / (e2e_ms * 1e-3), "unit": "slices/s", "ms_per_step": e2e_ms,
-                    "h2d_bytes_per_step": 8 * len(block), "d2h_bytes_per_step": 8 * M,
-                    "ms_each": [round(x, 2) for x in e2e_each]},
-            "roofline": roof,
-            "roofline_tensor": roof_tensor,
-            "kernel_ms_per_slice": {k: round(v["ms"], 4) for k, v in by_kind.items()},
-            "clocks": clocks,
-            "gpu_launches": args.steps * (len(block) * per_slice_launches + per_contract_launches) * (1 if block else 0),
+            "metric": METRIC, "value": main_r["value"], "unit": "slices/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": main_r["ms_per_step"], "higher_is_better": True,
+            "scaling": main_r["scaling"], "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+            "config": {**workload_config(cfg, main_r["per_step_slices"]),
+                       "slice_ids": f"{info['s']} global bits (2^{info['s']} slices), {info['s_local']} local bits "
+                                    f"summed inside each, {info['n_segments']} loop segments",
+                       "block_per_gpu": main_r["block"], "pipelines": main_r["pipes"],
+                       "parallelism": f"global slices / {world} GPUs",
+                       "l2": "flushed (512 MB write) before every timed step; workspace "
+                             f"{info['workspace_bytes'] / 2**30:.1f} GiB > L2",
+                       "setup_s": main_r["setup"]},
+            "complex_tflops": main_r["complex_tflops"],
+            "cmac_per_step": main_r["cmac_per_step"],
+            "plan_total_cmac": info["total_cmac"],
+            "time_to_M_amplitudes_s": main_r["extrap"]["seconds"],
+            "time_to_M_amplitudes": main_r["extrap"],
+            "e2e": main_r["e2e"],
+            "roofline": main_r["roofline"],
+            "roofline_tensor": main_r["roofline_tensor"],
+            "kernel_share": main_r["kernel_share"],
+            "segment_runs_per_step": main_r["segment_runs_per_step"],
+            "clocks": main_r["clocks"],
+            "gpu_launches": main_r["gpu_launches"],
             "cpu_baseline": cpu,
+            "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

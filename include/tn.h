@@ -190,7 +190,9 @@ tn_status tn_contract(tn_ctx* ctx, const uint64_t* slice_ids, int64_t n_ids, voi
                       int32_t out_on_device, double* seconds_out);
 
 /* Per-launch device times of one slice, for roofline accounting (CUDA events around every
- * launch on the bound stream, no graph).  Fills up to max_stats entries. */
+ * launch on the bound stream, no graph).  Loop programs: one pass through every segment at the slice's
+ * first local value (a segment's share of a full run is its time x its runs, tn_segment_runs).  Fills up
+ * to max_stats entries. */
 typedef struct {
     int32_t kind;        /* 0 instantiate, 1 apply (SIMT contraction), 2 gemm pre-pass A,
                             3 gemm pre-pass B, 4 tcgen05 gemm, 5 readout+accumulate, 6 permute,
@@ -200,9 +202,17 @@ typedef struct {
     double bytes;        /* algorithmic bytes of the launch                                    */
     double ms;           /* measured device time                                               */
     int64_t m, n, k, rows;
+    int32_t seg;         /* loop program: segment of the launch (-1: flat program)                */
+    int32_t pad;
 } tn_launch_stat;
 tn_status tn_profile_slice(tn_ctx* ctx, uint64_t slice_id, tn_launch_stat* stats, int32_t max_stats,
                            int32_t* n_stats);
+
+/* tn_segment_runs -- loop programs: how often each segment runs when tn_contract is called with the given
+ * slice ids on this ctx's bound pipelines (the executor's own enumeration, without launching anything).
+ * runs[j] for j < n_segments (tn_plan_info.n_segments; flat programs: 1 segment = one run per slice).
+ * EINVAL before tn_bind_device or on bad ids. */
+tn_status tn_segment_runs(tn_ctx* ctx, const uint64_t* slice_ids, int64_t n_ids, int64_t* runs);
 
 /* tn_sample -- host.  One sample per group of l bitstrings: exact categorical
  * draw with weights |a|^2 (frugal within the group), u = top 53 bits of a

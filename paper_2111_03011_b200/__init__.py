@@ -24,7 +24,7 @@ LIB_PATH = os.path.join(_HERE, "libtnb200.so")
 
 TN_OK, TN_EINVAL, TN_EINFEASIBLE, TN_ENUMERIC, TN_ECUDA, TN_ENOMEM = 0, 2, 3, 4, 5, 6
 KIND_NAMES = {0: "instantiate", 1: "apply", 2: "prep_a", 3: "prep_b", 4: "gemm_tcgen05", 5: "readout", 6: "permute",
-              7: "multi"}
+              7: "multi", 8: "accum"}
 
 
 class TnError(RuntimeError):
@@ -67,7 +67,8 @@ class TnPlanInfo(ctypes.Structure):
 class TnLaunchStat(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("step", ctypes.c_int32), ("cmac", ctypes.c_double),
                 ("bytes", ctypes.c_double), ("ms", ctypes.c_double), ("m", ctypes.c_int64),
-                ("n", ctypes.c_int64), ("k", ctypes.c_int64), ("rows", ctypes.c_int64)]
+                ("n", ctypes.c_int64), ("k", ctypes.c_int64), ("rows", ctypes.c_int64), ("seg", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
 
 
 class TnReport(ctypes.Structure):
@@ -75,7 +76,7 @@ class TnReport(ctypes.Structure):
                 ("f", "F_norm", "xeb", "log_xeb", "entropy_samples", "entropy_state", "pt_ks")]
 
 
-EXPORTS = ["tn_build", "tn_build_drilled", "tn_plan", "tn_plan_dump", "tn_plan_save", "tn_bind_device", "tn_contract", "tn_profile_slice",
+EXPORTS = ["tn_build", "tn_build_drilled", "tn_plan", "tn_plan_dump", "tn_plan_save", "tn_segment_runs", "tn_bind_device", "tn_contract", "tn_profile_slice",
            "tn_sample", "tn_sample_report", "tn_destroy", "tn_last_error", "tn_version", "tn_debug_gemm_tf32x3",
            "tn_debug_network", "tn_debug_launch_counts"]
 
@@ -101,6 +102,7 @@ def lib():
     L.tn_bind_device.argtypes = [c.c_void_p, c.c_int, c.c_void_p, c.c_size_t, c.c_void_p]
     L.tn_contract.argtypes = [c.c_void_p, P(c.c_uint64), c.c_int64, c.c_void_p, c.c_int32, P(c.c_double)]
     L.tn_profile_slice.argtypes = [c.c_void_p, c.c_uint64, P(TnLaunchStat), c.c_int32, P(c.c_int32)]
+    L.tn_segment_runs.argtypes = [c.c_void_p, P(c.c_uint64), c.c_int64, P(c.c_int64)]
     L.tn_sample.argtypes = [c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_uint64, P(c.c_uint64),
                             P(c.c_double)]
     L.tn_sample_report.argtypes = [c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_uint64, c.c_int32, c.c_int32,
@@ -114,7 +116,7 @@ def lib():
                                        c.c_int32, c.c_void_p]
     L.tn_debug_network.argtypes = [c.c_void_p, P(c.c_int64), P(c.c_int64), P(c.c_int64)]
     L.tn_debug_launch_counts.argtypes = [c.c_void_p, P(c.c_int64), P(c.c_int64)]
-    for name in ("tn_build", "tn_build_drilled", "tn_plan", "tn_plan_dump", "tn_plan_save", "tn_bind_device", "tn_contract", "tn_profile_slice",
+    for name in ("tn_build", "tn_build_drilled", "tn_plan", "tn_plan_dump", "tn_plan_save", "tn_segment_runs", "tn_bind_device", "tn_contract", "tn_profile_slice",
                  "tn_sample", "tn_sample_report", "tn_debug_gemm_tf32x3", "tn_debug_network", "tn_debug_launch_counts"):
         getattr(L, name).restype = c.c_int
     _lib = L
@@ -298,7 +300,15 @@ class SparseState:
         n = ctypes.c_int32(0)
         self._check(lib().tn_profile_slice(self._ctx, slice_id, arr, max_stats, ctypes.byref(n)))
         return [{"kind": KIND_NAMES.get(a.kind, str(a.kind)), "step": a.step, "cmac": a.cmac, "bytes": a.bytes,
-                 "ms": a.ms, "m": a.m, "n": a.n, "k": a.k, "rows": a.rows} for a in arr[:n.value]]
+                 "ms": a.ms, "m": a.m, "n": a.n, "k": a.k, "rows": a.rows, "seg": a.seg} for a in arr[:n.value]]
+
+    def segment_runs(self, slice_ids: Iterable[int]) -> List[int]:
+        """tn_segment_runs: runs of every loop-program segment for a tn_contract over slice_ids."""
+        ids = np.ascontiguousarray(np.fromiter((int(x) for x in slice_ids), dtype=np.uint64))
+        runs = np.zeros(max(1, self.info["n_segments"]), dtype=np.int64)
+        self._check(lib().tn_segment_runs(self._ctx, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(ids),
+                                          runs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+        return [int(x) for x in runs]
 
     # -------------------------------------------------------------- tn_sample
     def sample(self, amps: np.ndarray, n_slices_summed: int, seed: int, ideal: Optional[np.ndarray] = None):

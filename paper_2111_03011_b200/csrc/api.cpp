@@ -295,6 +295,20 @@ tn_status tn_contract(tn_ctx* ctx, const uint64_t* slice_ids, int64_t n_ids, voi
     return TN_OK;
 }
 
+tn_status tn_segment_runs(tn_ctx* ctx, const uint64_t* slice_ids, int64_t n_ids, int64_t* runs) {
+    if (!ctx || !runs) return TN_EINVAL;
+    if (!ctx->dev) return fail(ctx, TN_EINVAL, "tn_segment_runs before tn_bind_device");
+    if (!slice_ids || n_ids < 1) return fail(ctx, TN_EINVAL, "empty slice subset");
+    const int s = ctx->plan.segs.empty() ? (int)ctx->plan.sliced.size() : ctx->plan.n_global;
+    std::vector<uint64_t> ids(slice_ids, slice_ids + n_ids);
+    std::sort(ids.begin(), ids.end());
+    for (int64_t i = 0; i < n_ids; i++) {
+        if (s < 64 && ids[i] >= (1ull << s)) return fail(ctx, TN_EINVAL, "slice id out of range [0, 2^s)");
+        if (i && ids[i] == ids[i - 1]) return fail(ctx, TN_EINVAL, "duplicate slice id");
+    }
+    return (tn_status)tnb::dev_segment_runs(ctx->dev, ids.data(), n_ids, runs);
+}
+
 tn_status tn_profile_slice(tn_ctx* ctx, uint64_t slice_id, tn_launch_stat* stats, int32_t max_stats,
                            int32_t* n_stats) {
     if (!ctx || !stats || !n_stats) return TN_EINVAL;

@@ -1354,6 +1354,87 @@ static double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+struct LoopItem {
+    uint64_t tau;
+    int seg;
+    bool set;  // first segment run at this tau: write tau to the device first
+};
+
+// Loop programs: every pipeline enumerates the loop index tau in increasing order, its global bits restricted to
+// the pipeline's block of slice ids (a trie walk over the sorted block; global and local bits may interleave in
+// significance); a segment runs when all its Sum bits are 1 (the summations it reads are complete) and its D bits
+// differ from its previous run (else its kept outputs are still valid: head reuse across slices).
+static std::vector<std::vector<LoopItem>> loop_lists(const Device* d, const uint64_t* ids_sorted, int np,
+                                                     const std::vector<int64_t>& pstart,
+                                                     const std::vector<int64_t>& pcnt) {
+    const int s = d->s, J = (int)d->segm.size();
+    std::vector<int> gpos(s, -1);  // tau bit index (MSB first) -> global ordinal
+    int ng = 0;
+    for (int i = 0; i < s; i++)
+        if (d->bit_global[i]) gpos[i] = ng++;
+    std::vector<std::vector<LoopItem>> lists(np);
+    for (int p = 0; p < np; p++) {
+        if (pcnt[p] == 0) continue;
+        const uint64_t* blk = ids_sorted + pstart[p];
+        std::vector<uint64_t> last(J, 0);
+        std::vector<char> ran(J, 0);
+        std::vector<LoopItem>& out = lists[p];
+        std::function<void(int, uint64_t, int64_t, int64_t)> walk = [&](int i, uint64_t tau, int64_t lo, int64_t hi) {
+            if (i == s) {
+                bool set = false;
+                for (int j = 0; j < J; j++) {
+                    const Device::SegMask& g = d->segm[j];
+                    if ((tau & g.Sum) != g.Sum) continue;
+                    const uint64_t dv = tau & g.D;
+                    if (ran[j] && last[j] == dv) continue;
+                    out.push_back({tau, j, !set});
+                    set = true;
+                    ran[j] = 1;
+                    last[j] = dv;
+                }
+                return;
+            }
+            const uint64_t bit = 1ull << (s - 1 - i);
+            if (gpos[i] < 0) {
+                walk(i + 1, tau, lo, hi);
+                walk(i + 1, tau | bit, lo, hi);
+                return;
+            }
+            const int sh = ng - 1 - gpos[i];  // the block entries in [lo, hi) agree on the higher global bits
+            int64_t mid = lo;
+            while (mid < hi && !((blk[mid] >> sh) & 1)) mid++;
+            if (mid > lo) walk(i + 1, tau, lo, mid);
+            if (hi > mid) walk(i + 1, tau | bit, mid, hi);
+        };
+        walk(0, 0, 0, pcnt[p]);
+    }
+    return lists;
+}
+
+static void pipe_blocks(int64_t n, int np, std::vector<int64_t>& pstart, std::vector<int64_t>& pcnt) {
+    pstart.assign(np, 0);
+    pcnt.assign(np, 0);
+    for (int p = 0; p < np; p++) {  // contiguous block p of the ascending slice list (sizes differ by <= 1)
+        const int64_t base = n / np, extra = n % np;
+        pstart[p] = p * base + std::min<int64_t>(p, extra);
+        pcnt[p] = base + (p < extra ? 1 : 0);
+    }
+}
+
+int dev_segment_runs(Device* d, const uint64_t* ids_sorted, int64_t n, int64_t* runs) {
+    const int np = (int)std::min<int64_t>((int64_t)d->pipes.size(), n);
+    if (d->segm.empty()) {
+        runs[0] = n;
+        return TN_OK;
+    }
+    std::vector<int64_t> pstart, pcnt;
+    pipe_blocks(n, np, pstart, pcnt);
+    for (size_t j = 0; j < d->segm.size(); j++) runs[j] = 0;
+    for (const auto& L : loop_lists(d, ids_sorted, np, pstart, pcnt))
+        for (const LoopItem& it : L) runs[it.seg]++;
+    return TN_OK;
+}
+
 int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_out, bool out_dev, double* secs,
                  std::string& err) {
     static const bool trace = getenv("TNB_TRACE") != nullptr;
@@ -1370,13 +1451,8 @@ int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_ou
         CK(cudaEventRecord(d->evu, d->pre.stream));
     }
     std::vector<double2*> accs;
-    std::vector<int64_t> pstart(np), pcnt(np);
-    for (int p = 0; p < np; p++) {
-        // contiguous block p of the ascending slice list (sizes differ by <= 1)
-        const int64_t base = n / np, extra = n % np;
-        pstart[p] = p * base + std::min<int64_t>(p, extra);
-        pcnt[p] = base + (p < extra ? 1 : 0);
-    }
+    std::vector<int64_t> pstart, pcnt;
+    pipe_blocks(n, np, pstart, pcnt);
     for (int p = 0; p < np; p++) {
         Pipe& P = d->pipes[p];
         if (pcnt[p] == 0) continue;
@@ -1398,63 +1474,14 @@ int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_ou
             }
         }
     } else {
-        // loop program: every pipeline enumerates the loop index tau in increasing order, its global bits
-        // restricted to the pipeline's block of slice ids (a trie walk over the sorted block; global and
-        // local bits may interleave in significance); a segment runs when all its Sum bits are 1 (the
-        // summations it reads are complete) and its D bits differ from its previous run (else its kept
-        // outputs are still valid: head reuse).  Launches are issued round-robin over the pipelines.
-        const int s = d->s, J = (int)d->segm.size();
-        std::vector<int> gpos(s, -1);  // tau bit index (MSB first) -> global ordinal
-        int ng = 0;
-        for (int i = 0; i < s; i++)
-            if (d->bit_global[i]) gpos[i] = ng++;
-        struct Item {
-            uint64_t tau;
-            int seg;
-            bool set;
-        };
-        std::vector<std::vector<Item>> lists(np);
-        for (int p = 0; p < np; p++) {
-            if (pcnt[p] == 0) continue;
-            const uint64_t* blk = ids_sorted + pstart[p];
-            std::vector<uint64_t> last(J, 0);
-            std::vector<char> ran(J, 0);
-            std::vector<Item>& out = lists[p];
-            std::function<void(int, uint64_t, int64_t, int64_t)> walk = [&](int i, uint64_t tau, int64_t lo, int64_t hi) {
-                if (i == s) {
-                    bool set = false;
-                    for (int j = 0; j < J; j++) {
-                        const Device::SegMask& g = d->segm[j];
-                        if ((tau & g.Sum) != g.Sum) continue;
-                        const uint64_t dv = tau & g.D;
-                        if (ran[j] && last[j] == dv) continue;
-                        out.push_back({tau, j, !set});
-                        set = true;
-                        ran[j] = 1;
-                        last[j] = dv;
-                    }
-                    return;
-                }
-                const uint64_t bit = 1ull << (s - 1 - i);
-                if (gpos[i] < 0) {
-                    walk(i + 1, tau, lo, hi);
-                    walk(i + 1, tau | bit, lo, hi);
-                    return;
-                }
-                const int sh = ng - 1 - gpos[i];  // the block entries in [lo, hi) agree on the higher global bits
-                int64_t mid = lo;
-                while (mid < hi && !((blk[mid] >> sh) & 1)) mid++;
-                if (mid > lo) walk(i + 1, tau, lo, mid);
-                if (hi > mid) walk(i + 1, tau | bit, mid, hi);
-            };
-            walk(0, 0, 0, pcnt[p]);
-        }
+        // loop program: every pipeline enumerates the loop index tau (loop_lists), launches round-robin
+        std::vector<std::vector<LoopItem>> lists = loop_lists(d, ids_sorted, np, pstart, pcnt);
         for (size_t k = 0;; k++) {
             bool any = false;
             for (int p = 0; p < np; p++) {
                 if (k >= lists[p].size()) continue;
                 any = true;
-                const Item& it = lists[p][k];
+                const LoopItem& it = lists[p][k];
                 Pipe& P = d->pipes[p];
                 if (it.set) kern::k_set_tau<<<1, 1, 0, P.stream>>>(P.tau, it.tau);
                 CK(cudaGraphLaunch(P.seg[it.seg].gexec, P.stream));
@@ -1513,9 +1540,13 @@ int dev_profile(Device* d, uint64_t slice_id, tn_launch_stat* stats, int max_sta
     Pipe& P = d->pipes[0];
     // loop program: one pass through every segment at tau = slice_id << l (timing only)
     std::vector<std::pair<Pipe*, const Launch*>> seq;
+    std::vector<int> seqseg;
     if (d->segm.empty()) {
         CK(cudaMemcpyAsync(P.slice_ids, &slice_id, sizeof(uint64_t), cudaMemcpyHostToDevice, P.stream));
-        for (const Launch& L : P.launches) seq.push_back({&P, &L});
+        for (const Launch& L : P.launches) {
+            seq.push_back({&P, &L});
+            seqseg.push_back(-1);
+        }
     } else {
         uint64_t tau = 0;  // the slice id's bits at the global positions, local bits 0
         for (int i = 0, gk = 0; i < d->s; i++)
@@ -1524,8 +1555,11 @@ int dev_profile(Device* d, uint64_t slice_id, tn_launch_stat* stats, int max_sta
                 gk++;
             }
         kern::k_set_tau<<<1, 1, 0, P.stream>>>(P.tau, tau);
-        for (Pipe& C : P.seg)
-            for (const Launch& L : C.launches) seq.push_back({&C, &L});
+        for (size_t j = 0; j < P.seg.size(); j++)
+            for (const Launch& L : P.seg[j].launches) {
+                seq.push_back({&P.seg[j], &L});
+                seqseg.push_back((int)j);
+            }
     }
     CK(cudaMemsetAsync(P.counter, 0, sizeof(int64_t), P.stream));
     CK(cudaMemsetAsync(P.acc, 0, d->M * sizeof(double2), P.stream));
@@ -1554,6 +1588,8 @@ int dev_profile(Device* d, uint64_t slice_id, tn_launch_stat* stats, int max_sta
         s.n = L.n;
         s.k = L.k;
         s.rows = L.rows;
+        s.seg = seqseg[i];
+        s.pad = 0;
     }
     for (auto& e : ev) cudaEventDestroy(e);
     *n_stats = w;
