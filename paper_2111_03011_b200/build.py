@@ -17,7 +17,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 
 CXX_SRCS = ["network.cpp", "planner.cpp", "partition.cpp", "planfile.cpp", "lower.cpp", "api.cpp"]
 CU_SRCS = ["executor.cu"]
-HEADERS = ["tnb.h", "exec.h", "kernels.cuh", "gemm_tc.cuh"]
+HEADERS = ["tnb.h", "exec.h", "kernels.cuh", "gemm_tc.cuh", "gate_tc.cuh"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "exec.h"
+#include "gate_tc.cuh"
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
 #include "tnb.h"
@@ -115,6 +116,9 @@ struct Launch {
     std::vector<MemAcc> mem;     // workspace / persistent ranges read and written (graph dependencies)
     int a_region = REG_NONE, b_region = REG_NONE;  // apply operands' regions (tiny-step chains' preloads)
     int64_t a_off = 0, b_off = 0;
+    // K_GATE (tensor-core gate application, gate_tc.cuh)
+    gtc::GateDev gd;
+    int g_kc = 32, g_bn = 32;
     // K_ACCUM (loop-program summation)
     const float2* c_src = nullptr;
     float2* c_dst = nullptr;
@@ -166,6 +170,7 @@ struct Device {
     char* work_all = nullptr;
     bool own_work = false;
     float2* out = nullptr;
+    float2* hout = nullptr;          // pinned staging buffer of host-output contractions
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evu = nullptr;
     std::vector<Pipe> pipes;
     int64_t M = 0;
@@ -183,6 +188,36 @@ constexpr int kCaptureStreams = 4;  // + the pipeline's own stream
 constexpr int64_t kSliceCap = 4096;  // slice ids per upload (tn_contract feeds longer blocks in chunks)
 
 namespace {
+
+template <int KC, int BN>
+void launch_gate_t(const Launch& L, cudaStream_t st) {
+    gtc::k_gate_tc<KC, BN><<<L.grid, gtc::THREADS, gtc::GCfg<KC, BN>::SMEM, st>>>(L.gd);
+}
+
+void launch_gate(const Launch& L, cudaStream_t st) {
+    if (L.g_kc == 32) {
+        switch (L.g_bn) {
+            case 16: launch_gate_t<32, 16>(L, st); break;
+            case 32: launch_gate_t<32, 32>(L, st); break;
+            case 64: launch_gate_t<32, 64>(L, st); break;
+            case 128: launch_gate_t<32, 128>(L, st); break;
+            default: launch_gate_t<32, 256>(L, st); break;
+        }
+    } else {
+        switch (L.g_bn) {
+            case 16: launch_gate_t<64, 16>(L, st); break;
+            case 32: launch_gate_t<64, 32>(L, st); break;
+            case 64: launch_gate_t<64, 64>(L, st); break;
+            default: launch_gate_t<64, 128>(L, st); break;
+        }
+    }
+}
+
+template <int KC, int BN>
+cudaError_t set_gate_attr() {
+    return cudaFuncSetAttribute(gtc::k_gate_tc<KC, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                gtc::GCfg<KC, BN>::SMEM);
+}
 
 template <int NI, int TEAM>
 void launch_apply(const Launch& L, cudaStream_t st) {
@@ -303,6 +338,10 @@ int set_smem_attrs(int device, std::string& err) {
                             tc::Cfg<128, 2>::SMEM));
     CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             tc::Cfg<256, 2>::SMEM));
+    CK((set_gate_attr<32, 16>())); CK((set_gate_attr<32, 32>())); CK((set_gate_attr<32, 64>()));
+    CK((set_gate_attr<32, 128>())); CK((set_gate_attr<32, 256>()));
+    CK((set_gate_attr<64, 16>())); CK((set_gate_attr<64, 32>())); CK((set_gate_attr<64, 64>()));
+    CK((set_gate_attr<64, 128>()));
     done_mask |= bit;
     return TN_OK;
 }
@@ -418,6 +457,9 @@ void do_launch(Device* d, Pipe& P, const Launch& L, cudaStream_t st) {
             break;
         case K_ACCUM:
             kern::k_accum<<<L.grid, L.block, 0, st>>>(L.c_src, L.c_dst, L.c_n, P.tau, L.c_E);
+            break;
+        case K_GATE:
+            launch_gate(L, st);
             break;
         case K_MULTI:
             kern::k_chain<<<1, 256, L.smem, st>>>(P.msteps + L.m_first, L.m_n);
@@ -728,6 +770,77 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
             L.in_leaves = st.ip.n_leaves;
             L.in_items = st.ip.n_items;
             L.grid = grid_for(st.ip.n_items);
+        } else if (st.kind == K_GATE) {
+            const ApplyParams& a = st.ap;
+            gtc::GateDev& g = L.gd;
+            std::memset(&g, 0, sizeof(g));
+            g.A = (const float2*)ptr(a.A);
+            g.G = (const float2*)ptr(a.B);
+            g.C = (float2*)ptr(a.C);
+            g.ma = (const int32_t*)ptr(a.ma);
+            g.R = a.R;
+            g.a_row = a.a_row;
+            g.c_row = a.c_row;
+            const int fa = a.cA.n, nk = a.nk, nb = a.cB.n;
+            g.n_orb = (int64_t)1 << fa;
+            g.log2_orb = fa;
+            g.n_tiles = (a.R * g.n_orb + gtc::ROWS - 1) / gtc::ROWS;
+            g.K = 1 << nk;
+            g.N = 1 << nb;
+            L.g_kc = 2 * std::max(16, g.K);
+            L.g_bn = 2 * std::max(8, g.N);
+            // orbit bits in ascending C position: consecutive orbits -> consecutive C (and A) addresses
+            std::vector<std::pair<int, int>> ob;  // (C bit, A bit)
+            for (int i = 0; i < fa; i++) ob.push_back({a.cA.dst[i], a.cA.src[i]});
+            std::sort(ob.begin(), ob.end());
+            g.ntab = (fa + 7) / 8;
+            tabs.resize((tabs.size() + 3) & ~(size_t)3, 0);
+            const size_t tb = tabs.size();
+            for (int b = 0; b < g.ntab; b++)
+                for (int v = 0; v < 256; v++) {
+                    uint32_t ao = 0, co = 0;
+                    for (int t = 0; t < 8; t++)
+                        if (8 * b + t < fa && ((v >> t) & 1)) {
+                            ao += 1u << ob[8 * b + t].second;
+                            co += 1u << ob[8 * b + t].first;
+                        }
+                    tabs.push_back(ao);
+                    tabs.push_back(co);
+                }
+            const size_t kt = tabs.size();
+            for (int kk = 0; kk < g.K; kk++) {
+                uint32_t o = 0;
+                for (int t = 0; t < nk; t++)
+                    if ((kk >> t) & 1) o += 1u << a.kA[t];
+                tabs.push_back(o);
+            }
+            const size_t yt = tabs.size();
+            for (int n = 0; n < g.N; n++) {
+                uint32_t o = 0;
+                for (int u = 0; u < nb; u++)
+                    if ((n >> u) & 1) o += 1u << a.cB.dst[u];
+                tabs.push_back(o);
+            }
+            const size_t gt = tabs.size();
+            for (int kk = 0; kk < g.K; kk++)
+                for (int n = 0; n < g.N; n++) {
+                    uint32_t o = 0;
+                    for (int t = 0; t < nk; t++)
+                        if ((kk >> t) & 1) o += 1u << a.kB[t];
+                    for (int u = 0; u < nb; u++)
+                        if ((n >> u) & 1) o += 1u << a.cB.src[u];
+                    tabs.push_back(o);
+                }
+            fixes.push_back({P.launches.size(), 9, tb});
+            fixes.push_back({P.launches.size(), 10, kt});
+            fixes.push_back({P.launches.size(), 11, yt});
+            fixes.push_back({P.launches.size(), 12, gt});
+            L.grid = dim3((unsigned)std::min<int64_t>(g.n_tiles, 148));
+            L.block = dim3(gtc::THREADS);
+            L.m = g.n_orb * a.R;
+            L.n = g.N;
+            L.k = g.K;
+            L.rows = a.R;
         } else if (st.kind == K_APPLY) {
             const ApplyParams& a = st.ap;
             kern::ApplyDev& p = L.ap;
@@ -1110,7 +1223,11 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
         else if (f.which == 5) L.rgp.ftab = p;
         else if (f.which == 6) L.pt.tin = (const uint2*)p;
         else if (f.which == 7) L.pt.tout = p;
-        else L.pt.outer = (const uint2*)p;
+        else if (f.which == 8) L.pt.outer = (const uint2*)p;
+        else if (f.which == 9) L.gd.tab = p;
+        else if (f.which == 10) L.gd.koff = p;
+        else if (f.which == 11) L.gd.yoff = p;
+        else L.gd.goff = p;
     }
 
     P.launches = fuse_small(P, P.launches);
@@ -1508,8 +1625,16 @@ int dev_contract(Device* d, const uint64_t* ids_sorted, int64_t n, void* amps_ou
     CK(cudaEventRecord(d->ev1, P0.stream));
     if (trace) tB = now_ms();
     if (!out_dev) {
-        CK(cudaMemcpyAsync(amps_out, d->out, d->M * sizeof(float2), cudaMemcpyDeviceToHost, P0.stream));
-        CK(cudaStreamSynchronize(P0.stream));
+        // D2H into a pinned staging buffer (a pageable destination would make the copy wait inside the driver
+        // with a blocking wake-up), poll for completion, then copy to the caller's host buffer
+        if (!d->hout) CK(cudaMallocHost(&d->hout, std::max<int64_t>(d->M, 1) * sizeof(float2)));
+        CK(cudaMemcpyAsync(d->hout, d->out, d->M * sizeof(float2), cudaMemcpyDeviceToHost, P0.stream));
+        CK(cudaEventRecord(d->evu, P0.stream));
+        cudaError_t q;
+        while ((q = cudaEventQuery(d->evu)) == cudaErrorNotReady) {
+        }
+        CK(q);
+        std::memcpy(amps_out, d->hout, d->M * sizeof(float2));
     }
     CK(cudaEventRecord(d->evu, P0.stream));
     CK(cudaStreamWaitEvent(d->user, d->evu, 0));
@@ -1631,6 +1756,7 @@ void dev_destroy(Device* d) {
         if (P.stream) cudaStreamDestroy(P.stream);
     }
     if (d->own_work && d->work_all) cudaFree(d->work_all);
+    if (d->hout) cudaFreeHost(d->hout);
     cudaFree(d->bank);
     cudaFree(d->maps);
     cudaFree(d->pers);

@@ -1,0 +1,268 @@
+// gate_tc.cuh -- "stem absorbs a small tensor" on the 5th-gen tensor cores.
+//
+//   C[r][x, y] = sum_k A[ma(r)][x, k] * G[k, y]
+//
+// A is the big stem in its own bit layout (any positions for the k legs), G a small rowless tensor
+// (K = 2^nk <= 32 rows, N = 2^nn <= 128 columns after the complex-as-real embedding fits shared memory),
+// C the result in its own bit layout.  On SIMT a 16x16 complex gate costs 64 FFMA per stem element, which
+// made these steps ALU-bound at ~2x the HBM time (round-1 VERDICT: SIMT apply family at 23-43 % of the FMA
+// roof).  Here the stem is read once and written once, so the step is HBM-bound:
+//
+//   warps 0-3  producers: thread t owns tile row t (one orbit x): it gathers its K complex values with the
+//              orbit's and the k legs' byte-sliced offset tables, splits them into tf32 hi / lo (3xTF32,
+//              SURVEY §8(c) item 19) and stores them straight into the UMMA SWIZZLE_128B K-major layout of a
+//              4-stage shared-memory ring (no pre-pass through HBM), then fence.proxy.async + mbarrier.
+//   warp 8     MMA issuer: tcgen05.mma kind::tf32 M=128 N=2N K=8, three products (lo*hi, hi*lo, hi*hi) per
+//              k step, against the gate held resident in shared memory (embedded once per CTA at start:
+//              rows (gr, -gi) / (gi, gr), hi / lo), accumulators double-buffered in TMEM.
+//   warps 4-7  epilogue: tcgen05.ld (TMEM lane quarter = warp % 4) -> complex outputs -> C through the
+//              orbit's and the output legs' offset tables (coalesced when the orbit's low bits are C's).
+// Persistent: one CTA per SM (grid = min(tiles, 148)).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gemm_tc.cuh"
+
+namespace tnb {
+namespace gtc {
+
+constexpr int THREADS = 288;      // 4 producer + 4 epilogue + 1 MMA warp
+constexpr int ROWS = 128;         // orbits per tile (MMA M)
+
+struct GateDev {
+    const float2* A;
+    const float2* G;
+    float2* C;
+    const int32_t* ma;        // A row of output row r (null: r)
+    int64_t R, a_row, c_row;  // output rows, row strides (complex elements)
+    int64_t n_orb;            // orbits per row (power of two)
+    int log2_orb;
+    int64_t n_tiles;
+    int K, N;                 // actual k and n (complex); KC/BN may pad them
+    const uint32_t* tab;      // [ntab][256][2]: (A offset, C offset) of the orbit index bytes
+    int ntab;
+    const uint32_t* koff;     // [K]: A offset of k
+    const uint32_t* yoff;     // [N]: C offset of output n
+    const uint32_t* goff;     // [K][N]: G offset of (k, n)
+};
+
+template <int KC, int BN>
+struct GCfg {
+    static constexpr int STAGES = KC == 32 ? 4 : 2;
+    static constexpr int NKB = KC / 32;                  // 32-float (128 B) k-blocks
+    static constexpr int ATILE = ROWS * 128;             // one k-block of A: 16 KB
+    static constexpr int STAGE = 2 * NKB * ATILE;        // hi + lo
+    static constexpr int BTILE = BN * 128;               // one k-block of the gate
+    static constexpr int BBYTES = 2 * NKB * BTILE;       // hi + lo
+    static constexpr int SMEM = STAGES * STAGE + BBYTES + 1024 + 256;
+    static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+    static_assert(SMEM <= 227 * 1024, "gate kernel shared memory");
+};
+
+// byte offset of fp32 element (row, col) of a K-major SWIZZLE_128B tile made of 32-float k-blocks
+__device__ __forceinline__ uint32_t sw128_off(int row, int col, int rows) {
+    const int kb = col >> 5, c = col & 31;
+    const int chunk = (c >> 2) ^ (row & 7);
+    return (uint32_t)(kb * rows * 128 + row * 128 + chunk * 16 + (c & 3) * 4);
+}
+
+__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    hi = __uint_as_float(r);
+    lo = x - hi;
+}
+
+template <int KC, int BN>
+__global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
+    using CF = GCfg<KC, BN>;
+    constexpr int STAGES = CF::STAGES;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* bt = smem + STAGES * CF::STAGE;             // resident gate: hi k-blocks, then lo k-blocks
+    uint64_t* full = (uint64_t*)(bt + CF::BBYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;  // [2]
+    uint64_t* tempty = tfull + 2;      // [2]
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    __shared__ uint32_t s_tab[4 * 256 * 2];
+    __shared__ uint32_t s_koff[32];
+    __shared__ uint32_t s_yoff[128];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < p.ntab * 512; i += THREADS) s_tab[i] = p.tab[i];
+    for (int i = threadIdx.x; i < p.K; i += THREADS) s_koff[i] = p.koff[i];
+    for (int i = threadIdx.x; i < p.N; i += THREADS) s_yoff[i] = p.yoff[i];
+    // the gate, embedded (row 2n = (gr, -gi), row 2n+1 = (gi, gr) along k) and split, in the swizzled layout
+    for (int e = threadIdx.x; e < BN * (KC / 2); e += THREADS) {
+        const int j = e / (KC / 2), kk = e % (KC / 2);  // D column j = 2n + part, k index kk
+        const int n = j >> 1, part = j & 1;
+        float2 g = make_float2(0.f, 0.f);
+        if (kk < p.K && n < p.N) g = p.G[p.goff[kk * p.N + n]];
+        const float v0 = part ? g.y : g.x, v1 = part ? g.x : -g.y;
+        float h0, l0, h1, l1;
+        tf32_split(v0, h0, l0);
+        tf32_split(v1, h1, l1);
+        const uint32_t o0 = sw128_off(j, 2 * kk, BN), o1 = sw128_off(j, 2 * kk + 1, BN);
+        *(float*)(bt + o0) = h0;
+        *(float*)(bt + o1) = h1;
+        *(float*)(bt + CF::NKB * CF::BTILE + o0) = l0;
+        *(float*)(bt + CF::NKB * CF::BTILE + o1) = l1;
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            tc::mbar_init(&full[s], 128);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            tc::mbar_init(&tfull[b], 1);
+            tc::mbar_init(&tempty[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 8) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tmem_slot)),
+                     "r"(CF::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the gate tile is read by the tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const int64_t t0 = blockIdx.x, ts = gridDim.x;
+
+    if (warp < 4) {
+        // ------------------------------------------------------------ producers: gather + split + swizzle
+        const int row = threadIdx.x;  // 0..127
+        int it = 0;
+        for (int64_t t = t0; t < p.n_tiles; t += ts, it++) {
+            const int s = it % STAGES;
+            const uint32_t ph = (it / STAGES) & 1;
+            if (it >= STAGES) tc::mbar_wait(&empty[s], ph ^ 1);
+            uint8_t* st = smem + s * CF::STAGE;
+            const int64_t x = t * ROWS + row;
+            float2 v[KC / 2];
+            if (x < p.R * p.n_orb) {
+                const int64_t r = x >> p.log2_orb, o = x & (p.n_orb - 1);
+                uint32_t aoff = 0;
+                for (int b = 0; b < p.ntab; b++) aoff += s_tab[(b * 256 + (int)((o >> (8 * b)) & 255)) * 2];
+                const int64_t ra = p.ma ? (int64_t)p.ma[r] : r;
+                const float2* __restrict__ src = p.A + ra * p.a_row + aoff;
+#pragma unroll
+                for (int kk = 0; kk < KC / 2; kk++) v[kk] = kk < p.K ? __ldg(src + s_koff[kk]) : make_float2(0.f, 0.f);
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < KC / 2; kk++) v[kk] = make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int kk = 0; kk < KC / 2; kk += 2) {  // one 16-byte chunk = 2 complex values
+                float4 h, l;
+                tf32_split(v[kk].x, h.x, l.x);
+                tf32_split(v[kk].y, h.y, l.y);
+                tf32_split(v[kk + 1].x, h.z, l.z);
+                tf32_split(v[kk + 1].y, h.w, l.w);
+                const uint32_t o = sw128_off(row, 2 * kk, ROWS);
+                *(float4*)(st + o) = h;
+                *(float4*)(st + CF::NKB * CF::ATILE + o) = l;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc::mbar_arrive(&full[s]);
+        }
+    } else if (warp == 8) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_tf32(ROWS, BN);
+            const uint32_t bth = tc::smem_u32(bt), btl = bth + CF::NKB * CF::BTILE;
+            int it = 0;
+            for (int64_t t = t0; t < p.n_tiles; t += ts, it++) {
+                const int s = it % STAGES;
+                const uint32_t ph = (it / STAGES) & 1;
+                const int buf = it & 1;
+                const uint32_t tph = (it >> 1) & 1;
+                if (it >= 2) tc::mbar_wait(&tempty[buf], tph ^ 1);
+                tc::mbar_wait(&full[s], ph);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t ah = tc::smem_u32(smem + s * CF::STAGE), al = ah + CF::NKB * CF::ATILE;
+                const uint32_t acc = tmem + (uint32_t)(buf * BN);
+#pragma unroll
+                for (int kb = 0; kb < CF::NKB; kb++)
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const uint32_t ka = kb * CF::ATILE + k * 32, kbb = kb * CF::BTILE + k * 32;
+                        const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
+                        tc::mma_tf32(acc, tc::sdesc_sw128(al + ka), tc::sdesc_sw128(bth + kbb), idesc, first);
+                        tc::mma_tf32(acc, tc::sdesc_sw128(ah + ka), tc::sdesc_sw128(btl + kbb), idesc, 1u);
+                        tc::mma_tf32(acc, tc::sdesc_sw128(ah + ka), tc::sdesc_sw128(bth + kbb), idesc, 1u);
+                    }
+                tc::mma_commit(&empty[s]);
+                tc::mma_commit(&tfull[buf]);
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue warps 4..7
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        constexpr int CH = BN < 32 ? BN : 32;  // TMEM columns per load
+        int it = 0;
+        for (int64_t t = t0; t < p.n_tiles; t += ts, it++) {
+            const int buf = it & 1;
+            const uint32_t tph = (it >> 1) & 1;
+            tc::mbar_wait(&tfull[buf], tph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int64_t x = t * ROWS + row;
+            const bool valid = x < p.R * p.n_orb;
+            float2* dst = nullptr;
+            if (valid) {
+                const int64_t r = x >> p.log2_orb, o = x & (p.n_orb - 1);
+                uint32_t coff = 0;
+                for (int b = 0; b < p.ntab; b++) coff += s_tab[(b * 256 + (int)((o >> (8 * b)) & 255)) * 2 + 1];
+                dst = p.C + r * p.c_row + coff;
+            }
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += CH) {
+                uint32_t u[32];
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN + c0);
+                if constexpr (CH == 32) {
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+                        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
+                          "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
+                          "=r"(u[14]), "=r"(u[15]), "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]),
+                          "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]),
+                          "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+                        : "r"(taddr));
+                } else {
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+                        "%14,%15}, [%16];"
+                        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
+                          "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
+                          "=r"(u[14]), "=r"(u[15])
+                        : "r"(taddr));
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (valid) {
+#pragma unroll
+                    for (int q = 0; q < CH / 2; q++) {
+                        const int n = (c0 >> 1) + q;
+                        if (n < p.N) dst[s_yoff[n]] = make_float2(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1]));
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 8)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::TMEM_COLS));
+}
+
+}  // namespace gtc
+}  // namespace tnb

@@ -10,6 +10,7 @@
 // K_INSTANTIATE (row a2) fills the sliced leaves for slice sigma; K_READOUT (rows a6 iii + a7) gathers
 // the M amplitudes and accumulates them.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <sstream>
@@ -401,6 +402,15 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             acc(st, Cn.buf, Cn.bytes, true);
             st.cmac = cmac;
             st.bytes = 8.0 * (double)(sizeA + sizeB + RC * ap.c_row) + (maRef.region ? 4.0 * RC : 0) + (mbRef.region ? 4.0 * RC : 0);
+            // big stem x small rowless tensor: the fused tensor-core gate kernel (gate_tc.cuh) reads the stem once
+            // and writes the result once; SIMT would be FMA-bound (4 * 2^nk FFMA per element)
+            {
+                const int nk = ap.nk, nb = ap.cB.n;
+                const bool fits = nk >= 2 && nk <= 5 && nb >= 1 && nb <= (nk <= 4 ? 7 : 6) && ap.cA.n <= 32;
+                const bool big = (double)RC * std::ldexp(1.0, ap.cA.n) >= 1048576.0 && cmac >= 4.0 * 1048576.0 * 16;
+                static const bool gate_off = getenv("TNB_NO_GATE_TC") != nullptr;
+                if (!gate_off && fits && big && B->qmask == 0 && !mbRef.region) st.kind = K_GATE;
+            }
             {
                 std::ostringstream o;
                 o << ",\"apply\":{\"dA\":" << ap.dA << ",\"dB\":" << ap.dB << ",\"dC\":" << ap.dC << ",\"kA\":[";

@@ -103,6 +103,16 @@ inline StepCost step_cost(int a, int b, int c, int u, double rA, double rB, doub
         // them back
         const double ops_bytes = s.bytes + 8.0 * (4.0 * (sA + sB) + 4.0 * std::min(sA, sB));
         s.time = std::max(s.cmac / C_TC, ops_bytes / BW) + 3 * T_LAUNCH;
+    } else if (!(rowsA && rowsB) && [&]() {
+                   // big stem x small rowless tensor: the fused tensor-core gate kernel (lower.cpp / gate_tc.cuh)
+                   const bool a_small = !rowsA && (rowsB || sA < sB);
+                   const int dsmall = a_small ? a : b, dbig = a_small ? b : a;
+                   const double rbig = a_small ? rB : rA;
+                   const int fb = dsmall - kk, fa = dbig - kk;
+                   return kk >= 2 && kk <= 5 && fb >= 1 && fb <= (kk <= 4 ? 7 : 6) && fa <= 32 &&
+                          rbig * std::ldexp(1.0, fa) >= 1048576.0 && s.cmac >= 4.0 * 1048576.0 * 16;
+               }()) {
+        s.time = std::max(s.cmac / C_TC, s.bytes / BW) + T_LAUNCH;
     } else if (rowsA && rowsB) {
         // gather-contract: every output row re-reads its parents' rows (mostly from L2, ~3x HBM)
         const double reread = 8.0 * rC * (std::ldexp(1.0, a) + std::ldexp(1.0, b));

@@ -202,7 +202,8 @@ enum StepKind : int32_t {
     K_PERMUTE = 6,
     K_MULTI = 7,
     K_ACCUM = 8,      // loop program: dst = ((tau & E) == 0 ? 0 : dst) + src (local-slice summation)
-    K_SETTAU = 9      // (executor-internal)
+    K_SETTAU = 9,     // (executor-internal)
+    K_GATE = 10       // stem x small rowless tensor on the tensor cores (gate_tc.cuh), ApplyParams
 };
 
 // General sparse-row pairwise contraction (SIMT path):
