@@ -189,34 +189,50 @@ constexpr int64_t kSliceCap = 4096;  // slice ids per upload (tn_contract feeds 
 
 namespace {
 
-template <int KC, int BN>
+template <int KV, int BN>
 void launch_gate_t(const Launch& L, cudaStream_t st) {
-    gtc::k_gate_tc<KC, BN><<<L.grid, gtc::THREADS, gtc::GCfg<KC, BN>::SMEM, st>>>(L.gd);
+    constexpr int KC = KV >= 16 ? 2 * KV : 32;
+    gtc::k_gate_tc<KV, BN><<<L.grid, gtc::THREADS, gtc::GCfg<KC, BN>::SMEM, st>>>(L.gd);
 }
 
-void launch_gate(const Launch& L, cudaStream_t st) {
-    if (L.g_kc == 32) {
-        switch (L.g_bn) {
-            case 16: launch_gate_t<32, 16>(L, st); break;
-            case 32: launch_gate_t<32, 32>(L, st); break;
-            case 64: launch_gate_t<32, 64>(L, st); break;
-            case 128: launch_gate_t<32, 128>(L, st); break;
-            default: launch_gate_t<32, 256>(L, st); break;
-        }
-    } else {
-        switch (L.g_bn) {
-            case 16: launch_gate_t<64, 16>(L, st); break;
-            case 32: launch_gate_t<64, 32>(L, st); break;
-            case 64: launch_gate_t<64, 64>(L, st); break;
-            default: launch_gate_t<64, 128>(L, st); break;
-        }
+template <int KV>
+void launch_gate_k(const Launch& L, cudaStream_t st) {
+    switch (L.g_bn) {
+        case 16: launch_gate_t<KV, 16>(L, st); break;
+        case 32: launch_gate_t<KV, 32>(L, st); break;
+        case 64: launch_gate_t<KV, 64>(L, st); break;
+        case 128: launch_gate_t<KV, 128>(L, st); break;
+        default: if constexpr (KV <= 16) launch_gate_t<KV, 256>(L, st); break;
     }
 }
 
-template <int KC, int BN>
-cudaError_t set_gate_attr() {
-    return cudaFuncSetAttribute(gtc::k_gate_tc<KC, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+void launch_gate(const Launch& L, cudaStream_t st) {
+    switch (L.gd.K) {
+        case 4: launch_gate_k<4>(L, st); break;
+        case 8: launch_gate_k<8>(L, st); break;
+        case 16: launch_gate_k<16>(L, st); break;
+        default: launch_gate_k<32>(L, st); break;
+    }
+}
+
+template <int KV, int BN>
+cudaError_t set_gate_attr1() {
+    constexpr int KC = KV >= 16 ? 2 * KV : 32;
+    return cudaFuncSetAttribute(gtc::k_gate_tc<KV, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 gtc::GCfg<KC, BN>::SMEM);
+}
+
+template <int KV>
+cudaError_t set_gate_attr() {
+    cudaError_t e = cudaSuccess;
+    for (cudaError_t x : {set_gate_attr1<KV, 16>(), set_gate_attr1<KV, 32>(), set_gate_attr1<KV, 64>(),
+                          set_gate_attr1<KV, 128>()})
+        if (x != cudaSuccess) e = x;
+    if constexpr (KV <= 16) {
+        const cudaError_t x = set_gate_attr1<KV, 256>();
+        if (x != cudaSuccess) e = x;
+    }
+    return e;
 }
 
 template <int NI, int TEAM>
@@ -338,10 +354,7 @@ int set_smem_attrs(int device, std::string& err) {
                             tc::Cfg<128, 2>::SMEM));
     CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             tc::Cfg<256, 2>::SMEM));
-    CK((set_gate_attr<32, 16>())); CK((set_gate_attr<32, 32>())); CK((set_gate_attr<32, 64>()));
-    CK((set_gate_attr<32, 128>())); CK((set_gate_attr<32, 256>()));
-    CK((set_gate_attr<64, 16>())); CK((set_gate_attr<64, 32>())); CK((set_gate_attr<64, 64>()));
-    CK((set_gate_attr<64, 128>()));
+    CK(set_gate_attr<4>()); CK(set_gate_attr<8>()); CK(set_gate_attr<16>()); CK(set_gate_attr<32>());
     done_mask |= bit;
     return TN_OK;
 }
@@ -476,7 +489,7 @@ std::vector<Launch> fuse_small(Pipe& P, const std::vector<Launch>& in) {
     auto small = [&](const Launch& L) {
         return L.kind == K_APPLY && L.ap.ktab != nullptr && L.nob >= 0 && L.ap.nk <= 12 &&
                L.ap.R * L.ap.n_orbits <= fuse_max && L.cmac <= 4.0e6 &&
-               !L.ap.stage_b && !L.rows_mode && !L.na && !L.rg;
+               !L.ap.stage_b && !L.rows_mode && !L.na && !L.rg && !L.ap.rperm;
     };
     auto ov = [](const void* a, int64_t na, const void* b, int64_t nb) {
         const char* x = (const char*)a;
@@ -854,6 +867,7 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
             L.b_off = a.B.offset;
             p.ma = (const int32_t*)ptr(a.ma);
             p.mb = (const int32_t*)ptr(a.mb);
+            p.rperm = (const int32_t*)ptr(a.rperm);
             p.R = a.R;
             p.a_row = a.a_row;
             p.b_row = a.b_row;
@@ -1006,6 +1020,7 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                     q.C = p.C;
                     q.ma = p.ma;
                     q.mb = p.mb;
+                    q.rperm = p.rperm;
                     q.R = a.R;
                     q.a_row = a.a_row;
                     q.b_row = a.b_row;

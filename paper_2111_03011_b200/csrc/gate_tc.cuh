@@ -8,14 +8,15 @@
 // made these steps ALU-bound at ~2x the HBM time (round-1 VERDICT: SIMT apply family at 23-43 % of the FMA
 // roof).  Here the stem is read once and written once, so the step is HBM-bound:
 //
-//   warps 0-3  producers: thread t owns tile row t (one orbit x): it gathers its K complex values with the
-//              orbit's and the k legs' byte-sliced offset tables, splits them into tf32 hi / lo (3xTF32,
+//   warps 0-7  producers, in groups that fill consecutive stages: a thread owns 1-4 tile rows (orbits x) and
+//              gathers their K complex values with the orbit's and the k legs' byte-sliced offset tables (all
+//              loads issued before any use: >= 16 in flight per thread), splits them into tf32 hi / lo (3xTF32,
 //              SURVEY §8(c) item 19) and stores them straight into the UMMA SWIZZLE_128B K-major layout of a
-//              4-stage shared-memory ring (no pre-pass through HBM), then fence.proxy.async + mbarrier.
-//   warp 8     MMA issuer: tcgen05.mma kind::tf32 M=128 N=2N K=8, three products (lo*hi, hi*lo, hi*hi) per
+//              2-4-stage shared-memory ring (no pre-pass through HBM), then fence.proxy.async + mbarrier.
+//   warp 12    MMA issuer: tcgen05.mma kind::tf32 M=128 N=2N K=8, three products (lo*hi, hi*lo, hi*hi) per
 //              k step, against the gate held resident in shared memory (embedded once per CTA at start:
 //              rows (gr, -gi) / (gi, gr), hi / lo), accumulators double-buffered in TMEM.
-//   warps 4-7  epilogue: tcgen05.ld (TMEM lane quarter = warp % 4) -> complex outputs -> C through the
+//   warps 8-11 epilogue: tcgen05.ld (TMEM lane quarter = warp % 4) -> complex outputs -> C through the
 //              orbit's and the output legs' offset tables (coalesced when the orbit's low bits are C's).
 // Persistent: one CTA per SM (grid = min(tiles, 148)).
 #pragma once
@@ -28,7 +29,10 @@
 namespace tnb {
 namespace gtc {
 
-constexpr int THREADS = 288;      // 4 producer + 4 epilogue + 1 MMA warp
+constexpr int PROD = 256;         // producer threads (8 warps)
+constexpr int THREADS = PROD + 160;  // + 4 epilogue warps + 1 MMA warp
+constexpr int EPI0 = PROD / 32;      // first epilogue warp
+constexpr int MMAW = EPI0 + 4;       // MMA warp
 constexpr int ROWS = 128;         // orbits per tile (MMA M)
 
 struct GateDev {
@@ -75,8 +79,9 @@ __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
     lo = x - hi;
 }
 
-template <int KC, int BN>
+template <int KV, int BN>
 __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
+    constexpr int KC = KV >= 16 ? 2 * KV : 32;  // real K columns (K padded to >= 16 complex)
     using CF = GCfg<KC, BN>;
     constexpr int STAGES = CF::STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -111,9 +116,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
         *(float*)(bt + CF::NKB * CF::BTILE + o0) = l0;
         *(float*)(bt + CF::NKB * CF::BTILE + o1) = l1;
     }
+    // producer groups: each group of PG threads fills one stage (RPT rows per thread, >= 16 loads in flight per
+    // thread); NG = PROD / PG groups work on consecutive tiles, so NG stages are being filled at once
+    constexpr int RPT0 = KV >= 16 ? 1 : 16 / KV;
+    constexpr int RPT = RPT0 > ROWS * STAGES / PROD ? ROWS * STAGES / PROD : RPT0;
+    constexpr int PG = ROWS / RPT, NG = PROD / PG;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
-            tc::mbar_init(&full[s], 128);
+            tc::mbar_init(&full[s], PG);
             tc::mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; b++) {
@@ -122,7 +132,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 8) {
+    if (warp == MMAW) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tmem_slot)),
                      "r"(CF::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -134,44 +144,55 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
     const uint32_t tmem = *tmem_slot;
     const int64_t t0 = blockIdx.x, ts = gridDim.x;
 
-    if (warp < 4) {
+    if (warp < EPI0) {
         // ------------------------------------------------------------ producers: gather + split + swizzle
-        const int row = threadIdx.x;  // 0..127
-        int it = 0;
-        for (int64_t t = t0; t < p.n_tiles; t += ts, it++) {
+        const int g = threadIdx.x / PG, tid = threadIdx.x % PG;
+        int it = g;
+        for (int64_t t = t0 + (int64_t)g * ts; t < p.n_tiles; t += (int64_t)NG * ts, it += NG) {
             const int s = it % STAGES;
             const uint32_t ph = (it / STAGES) & 1;
             if (it >= STAGES) tc::mbar_wait(&empty[s], ph ^ 1);
             uint8_t* st = smem + s * CF::STAGE;
-            const int64_t x = t * ROWS + row;
-            float2 v[KC / 2];
-            if (x < p.R * p.n_orb) {
-                const int64_t r = x >> p.log2_orb, o = x & (p.n_orb - 1);
-                uint32_t aoff = 0;
-                for (int b = 0; b < p.ntab; b++) aoff += s_tab[(b * 256 + (int)((o >> (8 * b)) & 255)) * 2];
-                const int64_t ra = p.ma ? (int64_t)p.ma[r] : r;
-                const float2* __restrict__ src = p.A + ra * p.a_row + aoff;
+            float2 v[RPT * KV];
+            // issue every load of the stage first (16-32 in flight per thread), then split and store
 #pragma unroll
-                for (int kk = 0; kk < KC / 2; kk++) v[kk] = kk < p.K ? __ldg(src + s_koff[kk]) : make_float2(0.f, 0.f);
-            } else {
+            for (int rr = 0; rr < RPT; rr++) {
+                const int row = tid + rr * PG;
+                const int64_t x = t * ROWS + row;
+                if (x < p.R * p.n_orb) {
+                    const int64_t r = x >> p.log2_orb, o = x & (p.n_orb - 1);
+                    uint32_t aoff = 0;
+                    for (int b = 0; b < p.ntab; b++) aoff += s_tab[(b * 256 + (int)((o >> (8 * b)) & 255)) * 2];
+                    const int64_t ra = p.ma ? (int64_t)p.ma[r] : r;
+                    const float2* __restrict__ src = p.A + ra * p.a_row + aoff;
 #pragma unroll
-                for (int kk = 0; kk < KC / 2; kk++) v[kk] = make_float2(0.f, 0.f);
+                    for (int kk = 0; kk < KV; kk++) v[rr * KV + kk] = __ldg(src + s_koff[kk]);
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < KV; kk++) v[rr * KV + kk] = make_float2(0.f, 0.f);
+                }
             }
 #pragma unroll
-            for (int kk = 0; kk < KC / 2; kk += 2) {  // one 16-byte chunk = 2 complex values
-                float4 h, l;
-                tf32_split(v[kk].x, h.x, l.x);
-                tf32_split(v[kk].y, h.y, l.y);
-                tf32_split(v[kk + 1].x, h.z, l.z);
-                tf32_split(v[kk + 1].y, h.w, l.w);
-                const uint32_t o = sw128_off(row, 2 * kk, ROWS);
-                *(float4*)(st + o) = h;
-                *(float4*)(st + CF::NKB * CF::ATILE + o) = l;
+            for (int rr = 0; rr < RPT; rr++) {
+                const int row = tid + rr * PG;
+#pragma unroll
+                for (int kk = 0; kk < KC / 2; kk += 2) {  // one 16-byte chunk = 2 complex values (zero padding)
+                    const float2 a = kk < KV ? v[rr * KV + kk] : make_float2(0.f, 0.f);
+                    const float2 b = kk + 1 < KV ? v[rr * KV + kk + 1] : make_float2(0.f, 0.f);
+                    float4 h, l;
+                    tf32_split(a.x, h.x, l.x);
+                    tf32_split(a.y, h.y, l.y);
+                    tf32_split(b.x, h.z, l.z);
+                    tf32_split(b.y, h.w, l.w);
+                    const uint32_t o = sw128_off(row, 2 * kk, ROWS);
+                    *(float4*)(st + o) = h;
+                    *(float4*)(st + CF::NKB * CF::ATILE + o) = l;
+                }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             tc::mbar_arrive(&full[s]);
         }
-    } else if (warp == 8) {
+    } else if (warp == MMAW) {
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
             constexpr uint32_t idesc = tc::idesc_tf32(ROWS, BN);
@@ -202,7 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
             }
         }
     } else {
-        // ------------------------------------------------------------ epilogue warps 4..7
+        // ------------------------------------------------------------ epilogue warps EPI0 .. EPI0 + 3
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         constexpr int CH = BN < 32 ? BN : 32;  // TMEM columns per load
@@ -260,7 +281,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 8)
+    if (warp == MMAW)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::TMEM_COLS));
 }
 

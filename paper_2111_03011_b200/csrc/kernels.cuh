@@ -64,6 +64,8 @@ struct ApplyDev {
     int stage_b;           // 1: a 256-thread chunk lies in one output row; B's row is staged in smem
     int kparts;            // k_apply_rows: lanes sharing one orbit (power of two <= 32)
     uint32_t a_extra[4], c_extra[4];  // k_apply_na: offsets of the per-thread A-free C bits
+    const int32_t* rperm;  // output rows in processing order (grouped by A parent, so that re-reads of a shared
+                           // A row hit L2); null = ascending
 };
 constexpr int KTAB_MAX_BITS = 12;
 constexpr int STAGE_B_MAX = 4096;  // complex elements of B per row staged in shared memory
@@ -99,7 +101,8 @@ __global__ void __launch_bounds__(256, (NI == 4 && TEAM == 32) ? 2 : TNB_APPLY_M
         int64_t cached = -1;
         for (int64_t ch = ch0; ch < ch1; ch++) {
             const int64_t w = ch * per + threadIdx.x / TEAM;
-            const int64_t r = w / p.n_orbits;
+            const int64_t r0 = w / p.n_orbits;
+            const int64_t r = p.rperm ? (int64_t)p.rperm[r0] : r0;
             const int64_t rb = p.mb ? (int64_t)p.mb[r] : 0;
             if (rb != cached) {
                 __syncthreads();
@@ -108,7 +111,7 @@ __global__ void __launch_bounds__(256, (NI == 4 && TEAM == 32) ? 2 : TNB_APPLY_M
                 __syncthreads();
                 cached = rb;
             }
-            const int64_t o = w - r * p.n_orbits;
+            const int64_t o = w - r0 * p.n_orbits;
             uint32_t coff = 0, aoff = 0, boff = 0;
             for (int t = 0; t < p.ntab; t++) {
                 const uint32_t* e = sm + ((t << 8) + (int)((o >> (8 * t)) & 255)) * 4;
@@ -151,8 +154,9 @@ __global__ void __launch_bounds__(256, (NI == 4 && TEAM == 32) ? 2 : TNB_APPLY_M
     const int64_t team0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
     const int64_t nteams = ((int64_t)gridDim.x * blockDim.x) / TEAM;
     for (int64_t w = team0; w < total; w += nteams) {
-        const int64_t r = w / p.n_orbits;
-        const int64_t o = w - r * p.n_orbits;
+        const int64_t r0 = w / p.n_orbits;
+        const int64_t o = w - r0 * p.n_orbits;
+        const int64_t r = p.rperm ? (int64_t)p.rperm[r0] : r0;
         uint32_t coff = 0, aoff = 0, boff = 0;
         for (int t = 0; t < p.ntab; t++) {
             const uint32_t* e = sm + ((t << 8) + (int)((o >> (8 * t)) & 255)) * 4;
@@ -218,8 +222,9 @@ __global__ void __launch_bounds__(256) k_apply_na(const ApplyDev p) {
     const int64_t K = (int64_t)1 << p.nk;
     const int64_t total = p.R * p.n_orbits;
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = w / p.n_orbits;
-        const int64_t o = w - r * p.n_orbits;
+        const int64_t r0 = w / p.n_orbits;
+        const int64_t o = w - r0 * p.n_orbits;
+        const int64_t r = p.rperm ? (int64_t)p.rperm[r0] : r0;
         uint32_t coff = 0, aoff = 0, boff = 0;
         for (int t = 0; t < p.ntab; t++) {
             const uint32_t* e = sm + ((t << 8) + (int)((o >> (8 * t)) & 255)) * 4;
@@ -273,7 +278,8 @@ __global__ void __launch_bounds__(256) k_apply_rows(const ApplyDev p) {
     const int64_t K = (int64_t)1 << p.nk;
     const int kparts = p.kparts;
     const int64_t total_w = p.n_orbits * kparts;
-    for (int64_t r = blockIdx.x; r < p.R; r += gridDim.x) {
+    for (int64_t r0 = blockIdx.x; r0 < p.R; r0 += gridDim.x) {
+        const int64_t r = p.rperm ? (int64_t)p.rperm[r0] : r0;
         __syncthreads();
         const float2* Ag = p.A + (p.ma ? (int64_t)p.ma[r] : r) * p.a_row;
         const float2* Bg = p.B + (p.mb ? (int64_t)p.mb[r] : 0) * p.b_row;
@@ -465,6 +471,7 @@ struct RowGemmDev {
     int nk, fa, g;
     int nswz;
     int swz_src[4], swz_dst[4];  // B staging swizzle: bit dst of the smem index ^= bit src
+    const int32_t* rperm;        // output rows in processing order (null = ascending)
 };
 
 template <int FAT, int FB>
@@ -484,7 +491,8 @@ __global__ void __launch_bounds__(256, 2) k_apply_rg(const RowGemmDev p) {
     const int grp = threadIdx.x / tpg, tg = threadIdx.x % tpg;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int K = 1 << p.nk;
-    for (int64_t r = blockIdx.x; r < p.R; r += gridDim.x) {
+    for (int64_t r0 = blockIdx.x; r0 < p.R; r0 += gridDim.x) {
+        const int64_t r = p.rperm ? (int64_t)p.rperm[r0] : r0;
         const int64_t ra = p.ma ? (int64_t)p.ma[r] : r;
         const int64_t rb = p.mb ? (int64_t)p.mb[r] : 0;
         __syncthreads();  // the previous row is done with sB / red (and the tables are loaded)

@@ -362,6 +362,18 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             ap.ma = maRef;
             ap.mb = mbRef;
             ap.R = RC;
+            // several output rows read the same big A row: process them consecutively so that the re-reads hit
+            // L2 (gather-contract steps whose output rows are sorted by key, not by A parent)
+            if (maRef.region && ((int64_t)1 << A->legs.size()) >= 4096 && RC > (int64_t)A->rows.size()) {
+                bool mono = true;
+                for (int64_t r = 1; r < RC && mono; r++) mono = ma[r] >= ma[r - 1];
+                if (!mono) {
+                    std::vector<int32_t> perm(RC);
+                    for (int64_t r = 0; r < RC; r++) perm[r] = (int32_t)r;
+                    std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) { return ma[x] < ma[y]; });
+                    ap.rperm = BufRef{REG_MAPS, push_blob(prog.maps, perm.data(), perm.size() * 4)};
+                }
+            }
             ap.dA = (int)A->legs.size();
             ap.dB = (int)B->legs.size();
             ap.dC = (int)Cn.legs.size();
@@ -406,7 +418,10 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             // and writes the result once; SIMT would be FMA-bound (4 * 2^nk FFMA per element)
             {
                 const int nk = ap.nk, nb = ap.cB.n;
-                const bool fits = nk >= 2 && nk <= 5 && nb >= 1 && nb <= (nk <= 4 ? 7 : 6) && ap.cA.n <= 32;
+                // measured on config 4: 16x16 gates 3.5 ms (TC) vs 5.8 ms (SIMT) on a 2^30 stem; 8x8 gates are
+                // faster on SIMT (4.7 vs 5.6 ms), so small k needs a wide output to go to the tensor cores
+                const bool fits = nk >= 3 && nk <= 5 && nb >= 1 && nb <= (nk <= 4 ? 7 : 6) && ap.cA.n <= 32 &&
+                                  (nk >= 4 || nb >= 4);
                 const bool big = (double)RC * std::ldexp(1.0, ap.cA.n) >= 1048576.0 && cmac >= 4.0 * 1048576.0 * 16;
                 static const bool gate_off = getenv("TNB_NO_GATE_TC") != nullptr;
                 if (!gate_off && fits && big && B->qmask == 0 && !mbRef.region) st.kind = K_GATE;

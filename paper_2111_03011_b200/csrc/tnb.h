@@ -211,6 +211,7 @@ enum StepKind : int32_t {
 struct ApplyParams {
     BufRef A, B, C;
     BufRef ma, mb;            // int32 maps (REG_MAPS); region NONE: A identity, B row 0
+    BufRef rperm;             // int32 processing order of the output rows (grouped by A parent), or NONE
     int64_t R = 1;            // output rows
     int64_t a_row = 0, b_row = 0, c_row = 0;   // row strides in complex elements
     int dA = 0, dB = 0, dC = 0;
