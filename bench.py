@@ -275,13 +275,14 @@ def measure(args, T, torch, dist, dev, stream, cfg, rank, world, flush):
     M = ss.M
     out = torch.empty(M, dtype=torch.complex64, device=dev)
 
+    from paper_2111_03011_b200.dist import contract_distributed
+    all_ids = [x for rk in range(world) for x in (range(rk * B, (rk + 1) * B) if cfg.cfg >= 4 else [])] \
+        if cfg.cfg >= 4 else list(range(nS))
+
     def step(dst):
-        if block:
-            ss.contract(block, out=dst)
-        else:
-            dst.zero_()
-        if world > 1:
-            dist.all_reduce(torch.view_as_real(dst), op=dist.ReduceOp.SUM)
+        # the library's multi-GPU entry: this rank's contiguous block of the step's slice ids, then the
+        # all-reduce of the M amplitudes (plans were compared once above)
+        contract_distributed(ss, all_ids, out=dst, check_plan=False)
 
     for _ in range(args.warmup):
         step(out)
@@ -353,6 +354,16 @@ def measure(args, T, torch, dist, dev, stream, cfg, rank, world, flush):
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(tp)) if os.path.exists(tp) else []
     roof = roofline(dom[0], dom[1], pk, traffic)
+    # whole-step roofline: T_roof = sum over the step's launches of max(bytes / HBM, CMAC / C_peak),
+    # C_peak = the 3xTF32 complex ceiling (TF32 / 24 flops per CMAC), against the measured step time
+    c_peak = pk["bf16"] * (1.1 / 2.25) * 1e12 / 24.0
+    t_roof = 0.0
+    for p in prof:
+        w = runs[p["seg"]] if (loop and p["seg"] >= 0) else max(1, len(block))
+        t_roof += w * max(p["bytes"] / (pk["hbm_gbs"] * 1e9), p["cmac"] / c_peak)
+    whole = {"T_roof_ms": t_roof * 1e3, "T_meas_ms": ms_per_step, "frac": t_roof * 1e3 / ms_per_step,
+             "hbm_gbs": pk["hbm_gbs"], "c_peak_cmac_s": c_peak,
+             "note": "per rank; algorithmic bytes / CMAC of every launch weighted by its segment runs"}
     roof["share_of_step_serialized"] = dom[1]["w_ms"] / w_total
     roof_tensor = None
     if dom[0] != "gemm_tcgen05" and "gemm_tcgen05" in by_kind:
@@ -390,7 +401,7 @@ def measure(args, T, torch, dist, dev, stream, cfg, rank, world, flush):
                 "h2d_bytes_per_step": 8 * len(block) * world, "d2h_bytes_per_step": 8 * M * world,
                 "path": "tn_contract(out_on_device=0) + host all-reduce (gloo) for N > 1",
                 "ms_each": [round(x, 2) for x in e2e_each]},
-        "roofline": roof, "roofline_tensor": roof_tensor, "complex_tflops": 8.0 * cmac_step / (ms_per_step * 1e-3) / 1e12,
+        "roofline": roof, "roofline_tensor": roof_tensor, "whole_step_roofline": whole, "complex_tflops": 8.0 * cmac_step / (ms_per_step * 1e-3) / 1e12,
         "cmac_per_step": cmac_step, "extrap": extrap, "pipes": pipes,
         "kernel_share": {k: round(v["w_ms"] / w_total, 4) for k, v in by_kind.items()},
         "segment_runs_per_step": runs if loop else None,
@@ -450,6 +461,7 @@ def main():
         secondary = {"config": workload_config(c3, r3["per_step_slices"]), "value": r3["value"], "unit": "slices/s",
                      "ms_per_step": r3["ms_per_step"], "complex_tflops": r3["complex_tflops"], "e2e": r3["e2e"],
                      "roofline": r3["roofline"], "roofline_tensor": r3["roofline_tensor"],
+                     "whole_step_roofline": r3["whole_step_roofline"],
                      "kernel_share": r3["kernel_share"], "clocks": r3["clocks"], "setup_s": r3["setup"],
                      "pipelines": r3["pipes"], "gpu_launches": r3["gpu_launches"]}
         if rank == 0 and not args.no_cpu_baseline:
@@ -493,6 +505,7 @@ def main():
             "e2e": main_r["e2e"],
             "roofline": main_r["roofline"],
             "roofline_tensor": main_r["roofline_tensor"],
+            "whole_step_roofline": main_r["whole_step_roofline"],
             "kernel_share": main_r["kernel_share"],
             "segment_runs_per_step": main_r["segment_runs_per_step"],
             "clocks": main_r["clocks"],

@@ -797,11 +797,20 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
             const int fa = a.cA.n, nk = a.nk, nb = a.cB.n;
             g.n_orb = (int64_t)1 << fa;
             g.log2_orb = fa;
-            g.n_tiles = (a.R * g.n_orb + gtc::ROWS - 1) / gtc::ROWS;
+            g.mode = a.gate_mode;
+            g.perm = (const int32_t*)ptr(a.gperm);
+            g.mb = (const int32_t*)ptr(a.mb);
+            g.g_row = a.b_row;
+            g.gstart = (const int32_t*)ptr(a.gstart);
+            g.gcnt = (const int32_t*)ptr(a.gcnt);
+            g.GM = a.gm;
+            if (g.mode == 2) g.R = a.a_rows;  // tiles over A's rows
+            g.n_tiles = (g.R * g.n_orb + gtc::ROWS - 1) / gtc::ROWS;
             g.K = 1 << nk;
             g.N = 1 << nb;
+            const int ncols = (g.mode == 2 ? g.GM : 1) * g.N;
             L.g_kc = 2 * std::max(16, g.K);
-            L.g_bn = 2 * std::max(8, g.N);
+            L.g_bn = 2 * std::max(8, ncols);
             // orbit bits in ascending C position: consecutive orbits -> consecutive C (and A) addresses
             std::vector<std::pair<int, int>> ob;  // (C bit, A bit)
             for (int i = 0; i < fa; i++) ob.push_back({a.cA.dst[i], a.cA.src[i]});

@@ -49,7 +49,19 @@ struct GateDev {
     int ntab;
     const uint32_t* koff;     // [K]: A offset of k
     const uint32_t* yoff;     // [N]: C offset of output n
-    const uint32_t* goff;     // [K][N]: G offset of (k, n)
+    const uint32_t* goff;     // [K][N]: G offset of (k, n) within a G row
+    // gather-contract variants (both operands carry sparse rows, SURVEY a6 GATHER-CONTRACT)
+    int mode;                 // 0: one rowless gate G
+                              // 1: the gate of a tile is G's row mb[r] of its output row r; output rows are
+                              //    processed in perm order (grouped by B parent: the gate changes rarely)
+                              // 2: tiles run over A's rows (R = A rows); the gate's columns are (member i, n): the
+                              //    G rows of the output rows that share the tile's A row, so A is read once
+    const int32_t* perm;      // modes 1, 2: output rows in processing order
+    const int32_t* mb;        // modes 1, 2: G row of output row r
+    int64_t g_row;            // G row stride (complex elements)
+    const int32_t* gstart;    // mode 2: first perm position of A row a's output rows
+    const int32_t* gcnt;      // mode 2: their count (<= GM)
+    int GM;                   // mode 2: member slots per tile (gate columns = GM * N)
 };
 
 template <int KC, int BN>
@@ -91,31 +103,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;  // [2]
     uint64_t* tempty = tfull + 2;      // [2]
-    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    uint64_t* gfree = tempty + 2;      // [1]: the MMAs reading the resident gate have completed
+    uint32_t* tmem_slot = (uint32_t*)(gfree + 1);
     __shared__ uint32_t s_tab[4 * 256 * 2];
     __shared__ uint32_t s_koff[32];
     __shared__ uint32_t s_yoff[128];
+    __shared__ int64_t s_mrow[4][32];  // mode 2: output row offsets of the tile's members, per epilogue warp
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < p.ntab * 512; i += THREADS) s_tab[i] = p.tab[i];
     for (int i = threadIdx.x; i < p.K; i += THREADS) s_koff[i] = p.koff[i];
     for (int i = threadIdx.x; i < p.N; i += THREADS) s_yoff[i] = p.yoff[i];
-    // the gate, embedded (row 2n = (gr, -gi), row 2n+1 = (gi, gr) along k) and split, in the swizzled layout
-    for (int e = threadIdx.x; e < BN * (KC / 2); e += THREADS) {
-        const int j = e / (KC / 2), kk = e % (KC / 2);  // D column j = 2n + part, k index kk
-        const int n = j >> 1, part = j & 1;
-        float2 g = make_float2(0.f, 0.f);
-        if (kk < p.K && n < p.N) g = p.G[p.goff[kk * p.N + n]];
-        const float v0 = part ? g.y : g.x, v1 = part ? g.x : -g.y;
-        float h0, l0, h1, l1;
-        tf32_split(v0, h0, l0);
-        tf32_split(v1, h1, l1);
-        const uint32_t o0 = sw128_off(j, 2 * kk, BN), o1 = sw128_off(j, 2 * kk + 1, BN);
-        *(float*)(bt + o0) = h0;
-        *(float*)(bt + o1) = h1;
-        *(float*)(bt + CF::NKB * CF::BTILE + o0) = l0;
-        *(float*)(bt + CF::NKB * CF::BTILE + o1) = l1;
-    }
     // producer groups: each group of PG threads fills one stage (RPT rows per thread, >= 16 loads in flight per
     // thread); NG = PROD / PG groups work on consecutive tiles, so NG stages are being filled at once
     constexpr int RPT0 = KV >= 16 ? 1 : 16 / KV;
@@ -130,6 +128,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
             tc::mbar_init(&tfull[b], 1);
             tc::mbar_init(&tempty[b], 4);
         }
+        tc::mbar_init(gfree, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == MMAW) {
@@ -137,18 +136,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
                      "r"(CF::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the gate tile is read by the tensor core
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    const int64_t t0 = blockIdx.x, ts = gridDim.x;
+    // contiguous tile ranges per CTA: consecutive tiles share their gate (modes 1, 2), so reloads are rare
+    const int64_t tb = p.n_tiles * blockIdx.x / gridDim.x, te = p.n_tiles * (blockIdx.x + 1) / gridDim.x;
+    const int64_t total = p.R * p.n_orb;
+    // A row of a tile unit u (mode 2: u is the A row; else u is a perm position)
+    auto out_row = [&](int64_t u) -> int64_t { return p.perm ? (int64_t)p.perm[u] : u; };
 
     if (warp < EPI0) {
         // ------------------------------------------------------------ producers: gather + split + swizzle
         const int g = threadIdx.x / PG, tid = threadIdx.x % PG;
         int it = g;
-        for (int64_t t = t0 + (int64_t)g * ts; t < p.n_tiles; t += (int64_t)NG * ts, it += NG) {
+        for (int64_t t = tb + g; t < te; t += NG, it += NG) {
             const int s = it % STAGES;
             const uint32_t ph = (it / STAGES) & 1;
             if (it >= STAGES) tc::mbar_wait(&empty[s], ph ^ 1);
@@ -159,11 +161,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
             for (int rr = 0; rr < RPT; rr++) {
                 const int row = tid + rr * PG;
                 const int64_t x = t * ROWS + row;
-                if (x < p.R * p.n_orb) {
-                    const int64_t r = x >> p.log2_orb, o = x & (p.n_orb - 1);
+                if (x < total) {
+                    const int64_t u = x >> p.log2_orb, o = x & (p.n_orb - 1);
                     uint32_t aoff = 0;
                     for (int b = 0; b < p.ntab; b++) aoff += s_tab[(b * 256 + (int)((o >> (8 * b)) & 255)) * 2];
-                    const int64_t ra = p.ma ? (int64_t)p.ma[r] : r;
+                    int64_t ra = u;
+                    if (p.mode != 2) {
+                        const int64_t r = out_row(u);
+                        ra = p.ma ? (int64_t)p.ma[r] : r;
+                    }
                     const float2* __restrict__ src = p.A + ra * p.a_row + aoff;
 #pragma unroll
                     for (int kk = 0; kk < KV; kk++) v[rr * KV + kk] = __ldg(src + s_koff[kk]);
@@ -193,12 +199,50 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
             tc::mbar_arrive(&full[s]);
         }
     } else if (warp == MMAW) {
-        // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc = tc::idesc_tf32(ROWS, BN);
-            const uint32_t bth = tc::smem_u32(bt), btl = bth + CF::NKB * CF::BTILE;
-            int it = 0;
-            for (int64_t t = t0; t < p.n_tiles; t += ts, it++) {
+        // ------------------------------------------------------------ MMA issuer (+ gate loads)
+        constexpr uint32_t idesc = tc::idesc_tf32(ROWS, BN);
+        const uint32_t bth = tc::smem_u32(bt), btl = bth + CF::NKB * CF::BTILE;
+        int64_t cur = -1;
+        uint32_t gph = 0;
+        int it = 0;
+        for (int64_t t = tb; t < te; t++, it++) {
+            // the tile's gate: mode 0 one gate; mode 1 the G row of the tile's output row; mode 2 the tile's A row
+            const int64_t u0 = (t * ROWS) >> p.log2_orb;
+            const int64_t gid = p.mode == 0 ? 0 : (p.mode == 1 ? (int64_t)p.mb[out_row(u0)] : u0);
+            if (gid != cur) {
+                if (cur >= 0) {  // drain: every MMA that reads the resident gate has completed
+                    if (lane == 0) tc::mma_commit(gfree);
+                    tc::mbar_wait(gfree, gph);
+                    gph ^= 1;
+                }
+                // embedded gate (row 2n = (gr, -gi), row 2n+1 = (gi, gr) along k), split hi / lo, swizzled
+                const int members = p.mode == 2 ? p.gcnt[u0] : 1;
+                for (int e = lane; e < BN * (KC / 2); e += 32) {
+                    const int j = e / (KC / 2), kk = e % (KC / 2);  // D column j = 2 * (i * N + n) + part
+                    const int ne = j >> 1, part = j & 1;
+                    const int i = p.mode == 2 ? ne / p.N : 0, n = p.mode == 2 ? ne % p.N : ne;
+                    float2 g = make_float2(0.f, 0.f);
+                    if (kk < p.K && n < p.N && i < members) {
+                        int64_t grow = 0;
+                        if (p.mode == 1) grow = gid;
+                        else if (p.mode == 2) grow = p.mb[p.perm[p.gstart[u0] + i]];
+                        g = p.G[grow * p.g_row + p.goff[kk * p.N + n]];
+                    }
+                    const float v0 = part ? g.y : g.x, v1 = part ? g.x : -g.y;
+                    float h0, l0, h1, l1;
+                    tf32_split(v0, h0, l0);
+                    tf32_split(v1, h1, l1);
+                    const uint32_t o0 = sw128_off(j, 2 * kk, BN), o1 = sw128_off(j, 2 * kk + 1, BN);
+                    *(float*)(bt + o0) = h0;
+                    *(float*)(bt + o1) = h1;
+                    *(float*)(bt + CF::NKB * CF::BTILE + o0) = l0;
+                    *(float*)(bt + CF::NKB * CF::BTILE + o1) = l1;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                cur = gid;
+            }
+            if (lane == 0) {
                 const int s = it % STAGES;
                 const uint32_t ph = (it / STAGES) & 1;
                 const int buf = it & 1;
@@ -221,6 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
                 tc::mma_commit(&empty[s]);
                 tc::mma_commit(&tfull[buf]);
             }
+            __syncwarp();
         }
     } else {
         // ------------------------------------------------------------ epilogue warps EPI0 .. EPI0 + 3
@@ -228,19 +273,31 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
         const int row = quarter * 32 + lane;
         constexpr int CH = BN < 32 ? BN : 32;  // TMEM columns per load
         int it = 0;
-        for (int64_t t = t0; t < p.n_tiles; t += ts, it++) {
+        for (int64_t t = tb; t < te; t++, it++) {
             const int buf = it & 1;
             const uint32_t tph = (it >> 1) & 1;
             tc::mbar_wait(&tfull[buf], tph);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int64_t x = t * ROWS + row;
-            const bool valid = x < p.R * p.n_orb;
+            const bool valid = x < total;
+            uint32_t coff = 0;
+            int64_t uu = 0;
             float2* dst = nullptr;
             if (valid) {
-                const int64_t r = x >> p.log2_orb, o = x & (p.n_orb - 1);
-                uint32_t coff = 0;
+                uu = x >> p.log2_orb;
+                const int64_t o = x & (p.n_orb - 1);
                 for (int b = 0; b < p.ntab; b++) coff += s_tab[(b * 256 + (int)((o >> (8 * b)) & 255)) * 2 + 1];
-                dst = p.C + r * p.c_row + coff;
+                if (p.mode != 2) dst = p.C + out_row(uu) * p.c_row + coff;
+            }
+            int members = 0, lgN = 0;
+            if (p.mode == 2) {
+                // the members' output row offsets, one warp-level table per tile (a tile lies in one A row, so the
+                // whole warp shares them): one LDS per output instead of dependent global loads
+                const int64_t u0 = (t * ROWS) >> p.log2_orb;
+                members = p.gcnt[u0];
+                if (lane < members) s_mrow[quarter][lane] = (int64_t)p.perm[p.gstart[u0] + lane] * p.c_row;
+                __syncwarp();
+                lgN = 31 - __clz(p.N);
             }
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += CH) {
@@ -266,11 +323,19 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
                         : "r"(taddr));
                 }
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (valid) {
+                if (valid && p.mode != 2) {
 #pragma unroll
                     for (int q = 0; q < CH / 2; q++) {
                         const int n = (c0 >> 1) + q;
                         if (n < p.N) dst[s_yoff[n]] = make_float2(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1]));
+                    }
+                } else if (valid) {
+#pragma unroll
+                    for (int q = 0; q < CH / 2; q++) {
+                        const int ne = (c0 >> 1) + q, i = ne >> lgN, n = ne & (p.N - 1);
+                        if (i < members)
+                            p.C[s_mrow[quarter][i] + coff + s_yoff[n]] =
+                                make_float2(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1]));
                     }
                 }
             }

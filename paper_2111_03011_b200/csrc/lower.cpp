@@ -286,8 +286,9 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             const int64_t fb = (int64_t)B->legs.size() - (int64_t)K.size();
             const double cm = (double)RC * std::ldexp(1.0, (int)(fa + fb + K.size()));
             const int64_t RA = (int64_t)A->rows.size();
+            // (short k, <= 32, goes to the gate kernel's modes 1 / 2 below, which read A once without a pre-pass)
             grouped = K.size() >= 4 && fa >= 5 && cm >= 16.0 * 1024 * 1024 &&
-                      (RC >= 16 * RA || (fa >= 7 && RC >= 2 * RA));
+                      (RC >= 16 * RA || (fa >= 7 && RC >= 2 * RA)) && !(K.size() <= 5 && fa >= 7);
             if (!grouped && per_row(*B) > per_row(*A)) std::swap(A, B);  // SIMT: stream the larger rows
             use_gemm = grouped;
         } else {
@@ -425,6 +426,42 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
                 const bool big = (double)RC * std::ldexp(1.0, ap.cA.n) >= 1048576.0 && cmac >= 4.0 * 1048576.0 * 16;
                 static const bool gate_off = getenv("TNB_NO_GATE_TC") != nullptr;
                 if (!gate_off && fits && big && B->qmask == 0 && !mbRef.region) st.kind = K_GATE;
+                // gather-contract (both operands carry rows) on the gate kernel: A's orbits fill whole tiles
+                // (>= 128 per row).  Mode 2 when several output rows share an A row (A read once, the gate's
+                // columns are the group's B rows); mode 1 when few B rows serve many output rows (rows processed
+                // grouped by B parent, the resident gate reloaded at group boundaries)
+                const int64_t RA = (int64_t)A->rows.size(), RB = (int64_t)B->rows.size();
+                const bool gfit = nk >= 3 && nk <= 5 && ap.cA.n >= 7 && ap.cA.n <= 32 && B->qmask != 0 && mbRef.region;
+                if (!gate_off && gfit && big) {
+                    std::vector<int32_t> cnt(RA, 0);
+                    for (int64_t r = 0; r < RC; r++) cnt[ma[r]]++;
+                    const int gmax = *std::max_element(cnt.begin(), cnt.end());
+                    int gm = 1;
+                    while (gm < gmax) gm *= 2;
+                    const int ncols2 = gm << nb;  // complex gate columns in mode 2
+                    const int cap2 = nk <= 4 ? 128 : 64;
+                    if (RC >= 2 * RA && gm <= 16 && ncols2 <= cap2 && (nk >= 4 || ncols2 >= 16 || RC >= 3 * RA)) {
+                        std::vector<int32_t> perm(RC), gs(RA, 0);
+                        for (int64_t r = 0; r < RC; r++) perm[r] = (int32_t)r;
+                        std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) { return ma[x] < ma[y]; });
+                        for (int64_t a = 1; a < RA; a++) gs[a] = gs[a - 1] + cnt[a - 1];
+                        st.kind = K_GATE;
+                        st.ap.gate_mode = 2;
+                        st.ap.gm = gm;
+                        st.ap.a_rows = RA;
+                        st.ap.gperm = BufRef{REG_MAPS, push_blob(prog.maps, perm.data(), perm.size() * 4)};
+                        st.ap.gstart = BufRef{REG_MAPS, push_blob(prog.maps, gs.data(), gs.size() * 4)};
+                        st.ap.gcnt = BufRef{REG_MAPS, push_blob(prog.maps, cnt.data(), cnt.size() * 4)};
+                    } else if (RB * 8 <= RC && nb <= (nk <= 4 ? 7 : 6) && (nk >= 4 || nb >= 4)) {
+                        std::vector<int32_t> perm(RC);
+                        for (int64_t r = 0; r < RC; r++) perm[r] = (int32_t)r;
+                        std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) { return mb[x] < mb[y]; });
+                        st.kind = K_GATE;
+                        st.ap.gate_mode = 1;
+                        st.ap.a_rows = RA;
+                        st.ap.gperm = BufRef{REG_MAPS, push_blob(prog.maps, perm.data(), perm.size() * 4)};
+                    }
+                }
             }
             {
                 std::ostringstream o;
@@ -441,6 +478,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
                 o << "],\"ma\":" << (maRef.region ? 1 : 0) << ",\"mb\":" << (mbRef.region ? 1 : 0) << "}";
                 apply_json = o.str();
             }
+            if (st.kind == K_GATE) apply_json += ",\"gate_tc\":" + std::to_string(st.ap.gate_mode);
             out.push_back(st);
         } else {
             Cn.legs = fa;

@@ -113,6 +113,13 @@ inline StepCost step_cost(int a, int b, int c, int u, double rA, double rB, doub
                           rbig * std::ldexp(1.0, fa) >= 1048576.0 && s.cmac >= 4.0 * 1048576.0 * 16;
                }()) {
         s.time = std::max(s.cmac / C_TC, s.bytes / BW) + T_LAUNCH;
+    } else if (rowsA && rowsB && [&]() {
+                   // gather-contract on the gate kernel (modes 1 / 2, lower.cpp): the bigger-per-row operand's free
+                   // legs fill whole tiles, k fits the resident gate
+                   const int fa = std::max(a, b) - kk;
+                   return kk >= 3 && kk <= 5 && fa >= 7 && fa <= 32 && s.cmac >= 4.0 * 1048576.0 * 16;
+               }()) {
+        s.time = std::max(s.cmac / C_TC, s.bytes / BW) + T_LAUNCH;
     } else if (rowsA && rowsB) {
         // gather-contract: every output row re-reads its parents' rows (mostly from L2, ~3x HBM)
         const double reread = 8.0 * rC * (std::ldexp(1.0, a) + std::ldexp(1.0, b));

@@ -222,6 +222,12 @@ struct ApplyParams {
     int n_inner = 0;          // number of B-free C bits computed per thread (<= 4)
     int8_t inner_c[4];        // their C bit positions
     int64_t a_elems = 0, b_elems = 0;  // operand extents (complex elements), for hazard analysis
+    // K_GATE variants (gate_tc.cuh GateDev::mode): 1 = gate per B row (rows in gperm order), 2 = tiles over A rows
+    // with the gate columns = the B rows of the A row's output rows (gstart / gcnt per A row, <= gm members)
+    int gate_mode = 0;
+    BufRef gperm, gstart, gcnt;
+    int gm = 1;
+    int64_t a_rows = 0;
 };
 
 // Tensor-core path: TTGT with 3xTF32.
