@@ -211,7 +211,14 @@ def seg_dims(ss, info):
 
 
 def roofline(kind, d, pk, traffic):
-    if kind == "gemm_tcgen05":
+    if kind == "gate_tcgen05":
+        # tensor-core gate application (gate_tc.cuh): the stem is read once and the result written once, so the
+        # roof is HBM; algorithmic bytes = 8 (|A| + |G| + |C|)
+        bw = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+        r = {"bound": "hbm", "achieved": bw, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": bw / pk["hbm_gbs"],
+             "traffic": None, "kernel": "k_gate_tc", "peak_src": pk["src"],
+             "useful_complex_tflops": 8.0 * d["cmac"] / (d["ms"] * 1e-3) / 1e12}
+    elif kind == "gemm_tcgen05":
         # 3xTF32 tensor-core GEMM: 3 real GEMMs [Mp x 2K] x [2K x 2N] = 24 flops per complex MAC; peak = TF32
         # dense = measured bf16 x nominal tf32/bf16 ratio (1.1/2.25)
         achieved = 24.0 * d["cmac"] / (d["ms"] * 1e-3) / 1e12

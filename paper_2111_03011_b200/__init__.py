@@ -24,7 +24,7 @@ LIB_PATH = os.path.join(_HERE, "libtnb200.so")
 
 TN_OK, TN_EINVAL, TN_EINFEASIBLE, TN_ENUMERIC, TN_ECUDA, TN_ENOMEM = 0, 2, 3, 4, 5, 6
 KIND_NAMES = {0: "instantiate", 1: "apply", 2: "prep_a", 3: "prep_b", 4: "gemm_tcgen05", 5: "readout", 6: "permute",
-              7: "multi", 8: "accum"}
+              7: "multi", 8: "accum", 10: "gate_tcgen05"}
 
 
 class TnError(RuntimeError):

@@ -1192,6 +1192,9 @@ std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         S.nbr[a].push_back({b, e});
         S.nbr[b].push_back({a, e});
     }
+    // sweep objective: TNB_SWEEP_LOCAL=0 anneals under prefix caching only (every touched sliced edge stays open),
+    // which is what the laminar loop nest mostly reduces to when the stem keeps its sliced legs to the end
+    if (getenv("TNB_SWEEP_LOCAL")) S.local = atoi(getenv("TNB_SWEEP_LOCAL"));
     const int64_t iters = opt.sweep_iters > 0 ? opt.sweep_iters : std::max<int64_t>(20000, (int64_t)NL * 4000);
     const double pbudget = opt.persist_budget > 0 ? opt.persist_budget : 8.0 * opt.max_elems;
     auto peak_of = [&](const SweepState& x) {
