@@ -100,6 +100,8 @@ struct Launch {
     int gEA = 0;
     int gBN = 128;
     int gCG = 1;  // 2: CTA-pair tiles (cluster of 2, tcgen05 cta_group::2)
+    int gGA = 0;  // fused A pre-pass (gather producers)
+    tc::GatherA ga{};
     const int4* gTiles = nullptr;
     int gNTiles = 0, gTilesN = 1;
     const int32_t* gPerm = nullptr;
@@ -354,6 +356,16 @@ int set_smem_attrs(int device, std::string& err) {
                             tc::Cfg<128, 2>::SMEM));
     CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             tc::Cfg<256, 2>::SMEM));
+    CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<128, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            tc::Cfg<128>::SMEM_GA));
+    CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<64, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            tc::Cfg<64>::SMEM_GA));
+    CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<32, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            tc::Cfg<32>::SMEM_GA));
+    CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<128, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            tc::Cfg<128, 2>::SMEM_GA));
+    CK(cudaFuncSetAttribute(tc::k_gemm_tf32x3<256, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            tc::Cfg<256, 2>::SMEM_GA));
     CK(set_gate_attr<4>()); CK(set_gate_attr<8>()); CK(set_gate_attr<16>()); CK(set_gate_attr<32>());
     done_mask |= bit;
     return TN_OK;
@@ -386,12 +398,12 @@ size_t gemm_smem(int bn, int cg) {
     return bn == 128 ? tc::Cfg<128>::SMEM : (bn == 64 ? tc::Cfg<64>::SMEM : tc::Cfg<32>::SMEM);
 }
 
-template <int BN, int CG>
+template <int BN, int CG, bool GA = false>
 void launch_gemm_t(const Launch& L, cudaStream_t st) {
     if constexpr (CG == 1) {
-        tc::k_gemm_tf32x3<BN, 1><<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp,
-                                                                  L.gN2, L.gK2, L.gEA, L.gTiles, L.gPerm, L.gCm, L.gCn,
-                                                                  L.gNTiles, L.gTilesN);
+        tc::k_gemm_tf32x3<BN, 1, GA><<<L.grid, L.block, L.smem, st>>>(L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC,
+                                                                      L.gMp, L.gN2, L.gK2, L.gEA, L.gTiles, L.gPerm,
+                                                                      L.gCm, L.gCn, L.gNTiles, L.gTilesN, L.ga);
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = L.grid;
@@ -405,12 +417,25 @@ void launch_gemm_t(const Launch& L, cudaStream_t st) {
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        cudaLaunchKernelEx(&cfg, tc::k_gemm_tf32x3<BN, 2>, L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp, L.gN2,
-                           L.gK2, L.gEA, L.gTiles, L.gPerm, L.gCm, L.gCn, L.gNTiles, L.gTilesN);
+        cudaLaunchKernelEx(&cfg, tc::k_gemm_tf32x3<BN, 2, GA>, L.tm[0], L.tm[1], L.tm[2], L.tm[3], L.gC, L.gMp,
+                           L.gN2, L.gK2, L.gEA, L.gTiles, L.gPerm, L.gCm, L.gCn, L.gNTiles, L.gTilesN, L.ga);
     }
 }
 
 void launch_gemm(const Launch& L, cudaStream_t st) {
+    if (L.gGA) {
+        if (L.gCG == 2) {
+            if (L.gBN == 256) launch_gemm_t<256, 2, true>(L, st);
+            else launch_gemm_t<128, 2, true>(L, st);
+        } else if (L.gBN == 128) {
+            launch_gemm_t<128, 1, true>(L, st);
+        } else if (L.gBN == 64) {
+            launch_gemm_t<64, 1, true>(L, st);
+        } else {
+            launch_gemm_t<32, 1, true>(L, st);
+        }
+        return;
+    }
     if (L.gCG == 2) {
         if (L.gBN == 256) launch_gemm_t<256, 2>(L, st);
         else launch_gemm_t<128, 2>(L, st);
@@ -1202,9 +1227,49 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 const int64_t K2 = 2 * g.k;
                 const int64_t ncols = g.grouped ? g.NB * g.n : g.n;  // complex columns of the prepped B
                 const int64_t Dm = g.embed_a ? 2 * Mp : Mp, Dn = g.embed_a ? ncols : 2 * ncols;
-                if (!setup_gemm(L, ptr(g.Ahi), ptr(g.Alo), ptr(g.Bhi), ptr(g.Blo), Dm, Dn, K2, g.grouped != 0)) {
+                // gather_a: no A copies exist; the A maps are placeholders (never loaded)
+                const void* ahi = g.gather_a ? ptr(g.Bhi) : ptr(g.Ahi);
+                const void* alo = g.gather_a ? ptr(g.Blo) : ptr(g.Alo);
+                if (!setup_gemm(L, ahi, alo, ptr(g.Bhi), ptr(g.Blo), Dm, Dn, K2, g.grouped != 0)) {
                     err = "cuTensorMapEncodeTiled failed";
                     return TN_ECUDA;
+                }
+                if (g.gather_a) {
+                    L.gGA = 1;
+                    tc::GatherA& q = L.ga;
+                    q.A = (const float2*)ptr(g.A);
+                    q.ma = (const int32_t*)ptr(g.ma);
+                    q.a_row = g.a_row;
+                    q.Mp = Mp;
+                    q.log2m = lm;
+                    q.ntab = (lm + 7) / 8;
+                    q.K = (int)g.k;
+                    tabs.resize((tabs.size() + 3) & ~(size_t)3, 0);
+                    const size_t tm0 = tabs.size();
+                    for (int b = 0; b < q.ntab; b++)
+                        for (int v = 0; v < 256; v++) {
+                            uint32_t o = 0;
+                            for (int t = 0; t < 8; t++) {
+                                const int bit = 8 * b + t;  // m-index bit
+                                if (bit < lm && ((v >> t) & 1))
+                                    for (int u = 0; u < lm; u++)
+                                        if (g.aM.dst[u] == bit) o += 1u << g.aM.src[u];
+                            }
+                            tabs.push_back(o);
+                        }
+                    const size_t kt0 = tabs.size();
+                    for (int64_t kk = 0; kk < g.k; kk++) {
+                        uint32_t o = 0;
+                        for (int u = 0; u < lk; u++)
+                            if ((kk >> g.aK.dst[u]) & 1) o += 1u << g.aK.src[u];
+                        tabs.push_back(o);
+                    }
+                    fixes.push_back({P.launches.size(), 13, tm0});
+                    fixes.push_back({P.launches.size(), 14, kt0});
+                    L.block = dim3(tc::THREADS + tc::GA_PROD);
+                    L.smem = L.gCG == 2 ? (L.gBN == 256 ? tc::Cfg<256, 2>::SMEM_GA : tc::Cfg<128, 2>::SMEM_GA)
+                                        : (L.gBN == 128 ? tc::Cfg<128>::SMEM_GA
+                                                        : (L.gBN == 64 ? tc::Cfg<64>::SMEM_GA : tc::Cfg<32>::SMEM_GA));
                 }
                 L.gC = (float*)ptr(g.C);
                 L.gN2 = g.embed_a ? g.n : 2 * g.n;
@@ -1251,7 +1316,9 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
         else if (f.which == 9) L.gd.tab = p;
         else if (f.which == 10) L.gd.koff = p;
         else if (f.which == 11) L.gd.yoff = p;
-        else L.gd.goff = p;
+        else if (f.which == 12) L.gd.goff = p;
+        else if (f.which == 13) L.ga.tabm = p;
+        else L.ga.koff = p;
     }
 
     P.launches = fuse_small(P, P.launches);

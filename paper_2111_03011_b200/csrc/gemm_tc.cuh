@@ -40,6 +40,20 @@ constexpr int KSPLIT = 2;       // k-blocks alternate between KSPLIT accumulator
                                 // the tensor-core accumulator truncates, so shorter chains = less bias
 // BN (MMA N = rows of the B tile = real output columns per tile) is a template parameter: 128 for wide
 // contractions, 64 / 32 for tall-skinny ones (long K, few output columns).
+// Fused pre-pass for the plain (non-grouped, A-not-embedded) GEMM: 8 extra producer warps gather the A tile
+// straight from the stem in its own bit layout, split it into tf32 hi / lo and store it into the SWIZZLE_128B
+// layout (no K-major hi / lo copy of A through HBM); B keeps its TMA path.
+struct GatherA {
+    const float2* A;
+    const int32_t* ma;      // A row of output row r (null: r)
+    int64_t a_row, Mp;      // A row stride; D rows = R * 2^log2m
+    int log2m, ntab, K;     // m-index bits, byte tables, complex k
+    const uint32_t* tabm;   // [ntab][256]: A offsets of the m-index bytes
+    const uint32_t* koff;   // [K]: A offsets of k
+};
+constexpr int GA_PROD = 256;    // gather producer threads (2 groups of 128 rows, alternating stages)
+constexpr int GA_KMAX = 1024;   // koff table entries in shared memory
+
 template <int BN, int CG = 1>
 struct Cfg {
     static constexpr int BH = BN / CG;                              // B rows (MMA N) held by one CTA
@@ -47,6 +61,7 @@ struct Cfg {
     static constexpr int STAGE = 2 * TILE_BYTES + 2 * BTILE;        // Ahi, Alo, Bhi, Blo
     static constexpr int STAGES = (200 * 1024) / STAGE < 5 ? (200 * 1024) / STAGE : 5;
     static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int SMEM_GA = SMEM + 4 * 256 * 4 + GA_KMAX * 4;  // + gather tables
     static constexpr int KS = BN == 256 ? 1 : KSPLIT;               // accumulators per tile buffer
     static constexpr int TMEM_COLS = 2 * KS * BN;                   // 2 tile buffers x KS x BN columns
     static_assert(TMEM_COLS <= 512, "TMEM has 512 columns");
@@ -164,13 +179,13 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {  // arrive on t
         : "memory");
 }
 
-template <int BN, int CG = 1>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int BN, int CG = 1, bool GA = false>
+__global__ void __launch_bounds__(GA ? THREADS + GA_PROD : THREADS, 1)
     k_gemm_tf32x3(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                   const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
                   float* __restrict__ C, int64_t Mp, int64_t N2, int64_t K2, int ea,
                   const int4* __restrict__ tiles, const int32_t* __restrict__ perm, int64_t cm, int64_t cn,
-                  int n_tiles, int tiles_n) {
+                  int n_tiles, int tiles_n, const GatherA ga) {
     using CF = Cfg<BN, CG>;
     constexpr int STAGES = CF::STAGES;
     constexpr int STAGE_BYTES = CF::STAGE;
@@ -185,8 +200,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* tfull = empty + STAGES;   // [2]
     uint64_t* tempty = tfull + 2;       // [2]
     uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    uint32_t* s_tabm = (uint32_t*)((uint8_t*)full + 256);   // GA: gather tables after the barriers
+    uint32_t* s_koff = s_tabm + 4 * 256;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if constexpr (GA) {
+        for (int i = threadIdx.x; i < ga.ntab * 256; i += blockDim.x) s_tabm[i] = ga.tabm[i];
+        for (int i = threadIdx.x; i < ga.K; i += blockDim.x) s_koff[i] = ga.koff[i];
+    }
     const int nkb = (int)(K2 / BK);
     const uint32_t rank = CG == 2 ? cluster_rank() : 0u;       // CTA rank in the pair (0 = MMA leader)
     const int tile0 = (int)blockIdx.x / CG, tstride = (int)gridDim.x / CG;
@@ -195,7 +216,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
-            mbar_init(&full[s], 1);
+            // GA: the TMA thread's expect_tx arrive + one arrive per gather producer (of both CTAs of a pair)
+            mbar_init(&full[s], GA ? 1 + CG * (GA_PROD / 2) : 1);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; b++) {
@@ -275,19 +297,23 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if constexpr (CG == 2) {
                         // both CTAs' bytes complete on the leader's barrier; the leader arms it for both
                         const uint32_t fb = map_to_rank(&full[s], 0);
-                        if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+                        if (rank == 0) mbar_expect_tx(&full[s], GA ? 2 * 2 * CF::BTILE : 2 * STAGE_BYTES);
                         // grouped tiles run MMA N = the group's columns (rounded to 16): CTA r holds
                         // D columns [r * N/2, (r + 1) * N/2) of the tile
                         const int ntile = tiles ? min(BN, (yv + 15) & ~15) : BN;
                         const int nb = n0 + (int)rank * (ntile >> 1);
-                        tma_load_2d_pair(st + 0 * TILE_BYTES, &mAhi, fb, kc, m0);
-                        tma_load_2d_pair(st + 1 * TILE_BYTES, &mAlo, fb, kc, m0);
+                        if constexpr (!GA) {
+                            tma_load_2d_pair(st + 0 * TILE_BYTES, &mAhi, fb, kc, m0);
+                            tma_load_2d_pair(st + 1 * TILE_BYTES, &mAlo, fb, kc, m0);
+                        }
                         tma_load_2d_pair(st + B0, &mBhi, fb, kc, nb);
                         tma_load_2d_pair(st + B1, &mBlo, fb, kc, nb);
                     } else {
-                        mbar_expect_tx(&full[s], STAGE_BYTES);
-                        tma_load_2d(st + 0 * TILE_BYTES, &mAhi, &full[s], kc, m0);
-                        tma_load_2d(st + 1 * TILE_BYTES, &mAlo, &full[s], kc, m0);
+                        mbar_expect_tx(&full[s], GA ? 2 * CF::BTILE : STAGE_BYTES);
+                        if constexpr (!GA) {
+                            tma_load_2d(st + 0 * TILE_BYTES, &mAhi, &full[s], kc, m0);
+                            tma_load_2d(st + 1 * TILE_BYTES, &mAlo, &full[s], kc, m0);
+                        }
                         tma_load_2d(st + B0, &mBhi, &full[s], kc, n0);
                         tma_load_2d(st + B1, &mBlo, &full[s], kc, n0);
                     }
@@ -342,6 +368,61 @@ __global__ void __launch_bounds__(THREADS, 1)
                     mma_commit_pair(&tfull[buf]);  // accumulator halves ready for both epilogues
                 else
                     mma_commit(&tfull[buf]);
+            }
+        }
+    } else if (GA && warp >= THREADS / 32) {
+        if constexpr (GA) {
+            // -------------------------------------------------------- gather producers (fused A pre-pass)
+            const int pt = threadIdx.x - THREADS, g = pt >> 7, row = pt & 127;
+            const uint32_t fb0 = CG == 2 ? map_to_rank(&full[0], 0) : 0u;
+            int it = 0;
+            for (int t = tile0; t < n_tiles; t += tstride) {
+                int m0, n0, xv, xb, yv, yb, go;
+                tile_coords(t, m0, n0, xv, xb, yv, yb, go);
+                const int64_t x = (int64_t)m0 + row;
+                const float2* __restrict__ base = nullptr;
+                if (x < ga.Mp) {
+                    const int64_t r = x >> ga.log2m, mi = x & (((int64_t)1 << ga.log2m) - 1);
+                    uint32_t aoff = 0;
+                    for (int b = 0; b < ga.ntab; b++) aoff += s_tabm[b * 256 + (int)((mi >> (8 * b)) & 255)];
+                    base = ga.A + (ga.ma ? (int64_t)ga.ma[r] : r) * ga.a_row + aoff;
+                }
+                for (int kb = 0; kb < nkb; kb++, it++) {
+                    if ((it & 1) != g) continue;
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    if (it >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t* st = smem + s * STAGE_BYTES;
+                    float2 v[16];
+#pragma unroll
+                    for (int kk = 0; kk < 16; kk++) {
+                        const int k = kb * 16 + kk;
+                        v[kk] = (base && k < ga.K) ? __ldg(base + s_koff[k]) : make_float2(0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < 16; kk += 2) {
+                        float4 h, l;
+                        uint32_t r0;
+                        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r0) : "f"(v[kk].x));
+                        h.x = __uint_as_float(r0);
+                        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r0) : "f"(v[kk].y));
+                        h.y = __uint_as_float(r0);
+                        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r0) : "f"(v[kk + 1].x));
+                        h.z = __uint_as_float(r0);
+                        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r0) : "f"(v[kk + 1].y));
+                        h.w = __uint_as_float(r0);
+                        l = make_float4(v[kk].x - h.x, v[kk].y - h.y, v[kk + 1].x - h.z, v[kk + 1].y - h.w);
+                        const int c = 2 * kk;  // float column of this 16-byte chunk
+                        const uint32_t o = (uint32_t)(row * 128 + (((c >> 2) ^ (row & 7)) << 4));
+                        *(float4*)(st + o) = h;
+                        *(float4*)(st + TILE_BYTES + o) = l;
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    if constexpr (CG == 2)
+                        mbar_arrive_cluster(fb0 + (uint32_t)(s * sizeof(uint64_t)));
+                    else
+                        mbar_arrive(&full[s]);
+                }
             }
         }
     } else {

@@ -590,8 +590,13 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             }
             const int64_t abytes = (gp.embed_a ? 2 : 1) * Mp * 2 * k * 4,
                           bbytes = (gp.embed_a ? 1 : 2) * NBcols * 2 * k * 4;
-            gp.Ahi = BufRef{reg, al.alloc(abytes)};
-            gp.Alo = BufRef{reg, al.alloc(abytes)};
+            // fused A pre-pass (plain GEMMs with A on the plain side): the GEMM gathers and splits A itself
+            static const bool ga_off = getenv("TNB_NO_GATHER_A") != nullptr;
+            gp.gather_a = (!ga_off && !grouped && !gp.embed_a && k <= 1024 && fa.size() <= 32) ? 1 : 0;
+            if (!gp.gather_a) {
+                gp.Ahi = BufRef{reg, al.alloc(abytes)};
+                gp.Alo = BufRef{reg, al.alloc(abytes)};
+            }
             gp.Bhi = BufRef{reg, al.alloc(bbytes)};
             gp.Blo = BufRef{reg, al.alloc(bbytes)};
             Cn.bytes = RC * m * n * 8;
@@ -613,22 +618,30 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             sg.gp = gp;
             sg.cmac = cmac;
             sg.bytes = 2.0 * abytes + 2.0 * bbytes + 8.0 * RC * m * n;
-            acc(sa, A->buf, sizeA * 8, false);
-            acc(sa, gp.Ahi, abytes, true);
-            acc(sa, gp.Alo, abytes, true);
             acc(sb, B->buf, sizeB * 8, false);
             acc(sb, gp.Bhi, bbytes, true);
             acc(sb, gp.Blo, bbytes, true);
-            acc(sg, gp.Ahi, abytes, false);
-            acc(sg, gp.Alo, abytes, false);
             acc(sg, gp.Bhi, bbytes, false);
             acc(sg, gp.Blo, bbytes, false);
             acc(sg, Cn.buf, Cn.bytes, true);
-            out.push_back(sa);
+            if (gp.gather_a) {
+                sg.gp = gp;
+                sg.bytes = 8.0 * Mp * k + 2.0 * bbytes + 8.0 * RC * m * n;
+                acc(sg, A->buf, sizeA * 8, false);
+            } else {
+                acc(sa, A->buf, sizeA * 8, false);
+                acc(sa, gp.Ahi, abytes, true);
+                acc(sa, gp.Alo, abytes, true);
+                acc(sg, gp.Ahi, abytes, false);
+                acc(sg, gp.Alo, abytes, false);
+                out.push_back(sa);
+            }
             out.push_back(sb);
             out.push_back(sg);
-            al.release(gp.Ahi.offset, abytes);
-            al.release(gp.Alo.offset, abytes);
+            if (!gp.gather_a) {
+                al.release(gp.Ahi.offset, abytes);
+                al.release(gp.Alo.offset, abytes);
+            }
             al.release(gp.Bhi.offset, bbytes);
             al.release(gp.Blo.offset, bbytes);
             if (var) prog.gemm_cmac += cmac;
