@@ -116,7 +116,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
     for (int i = threadIdx.x; i < p.N; i += THREADS) s_yoff[i] = p.yoff[i];
     // producer groups: each group of PG threads fills one stage (RPT rows per thread, >= 16 loads in flight per
     // thread); NG = PROD / PG groups work on consecutive tiles, so NG stages are being filled at once
-    constexpr int RPT0 = KV >= 16 ? 1 : 16 / KV;
+    // >= 32 loads in flight per producer thread where the ring allows it (ncu: the kernel is long-scoreboard
+    // bound at 1 row x 16 loads per thread)
+    constexpr int RPT0 = KV >= 32 ? 1 : 32 / KV;
     constexpr int RPT = RPT0 > ROWS * STAGES / PROD ? ROWS * STAGES / PROD : RPT0;
     constexpr int PG = ROWS / RPT, NG = PROD / PG;
     if (threadIdx.x == 0) {
