@@ -854,18 +854,29 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                     tabs.push_back(ao);
                     tabs.push_back(co);
                 }
+            // k legs and output legs in index order; the leg on A's bit 0 (C's bit 0) goes first, so that k
+            // (n) pairs (2i, 2i+1) are adjacent in memory: 16-byte loads (stores)
+            std::vector<int> ko(nk), no(nb);
+            for (int t = 0; t < nk; t++) ko[t] = t;
+            for (int u = 0; u < nb; u++) no[u] = u;
+            for (int t = 0; t < nk; t++)
+                if (a.kA[t] == 0) std::swap(ko[0], ko[t]);
+            for (int u = 0; u < nb; u++)
+                if (a.cB.dst[u] == 0) std::swap(no[0], no[u]);
+            g.kpair = (nk >= 1 && a.kA[ko[0]] == 0) ? 1 : 0;
+            g.ypair = (nb >= 1 && a.cB.dst[no[0]] == 0 && g.mode != 2) ? 1 : 0;
             const size_t kt = tabs.size();
             for (int kk = 0; kk < g.K; kk++) {
                 uint32_t o = 0;
                 for (int t = 0; t < nk; t++)
-                    if ((kk >> t) & 1) o += 1u << a.kA[t];
+                    if ((kk >> t) & 1) o += 1u << a.kA[ko[t]];
                 tabs.push_back(o);
             }
             const size_t yt = tabs.size();
             for (int n = 0; n < g.N; n++) {
                 uint32_t o = 0;
                 for (int u = 0; u < nb; u++)
-                    if ((n >> u) & 1) o += 1u << a.cB.dst[u];
+                    if ((n >> u) & 1) o += 1u << a.cB.dst[no[u]];
                 tabs.push_back(o);
             }
             const size_t gt = tabs.size();
@@ -873,9 +884,9 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 for (int n = 0; n < g.N; n++) {
                     uint32_t o = 0;
                     for (int t = 0; t < nk; t++)
-                        if ((kk >> t) & 1) o += 1u << a.kB[t];
+                        if ((kk >> t) & 1) o += 1u << a.kB[ko[t]];
                     for (int u = 0; u < nb; u++)
-                        if ((n >> u) & 1) o += 1u << a.cB.src[u];
+                        if ((n >> u) & 1) o += 1u << a.cB.src[no[u]];
                     tabs.push_back(o);
                 }
             fixes.push_back({P.launches.size(), 9, tb});

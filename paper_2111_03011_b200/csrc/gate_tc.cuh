@@ -45,6 +45,7 @@ struct GateDev {
     int log2_orb;
     int64_t n_tiles;
     int K, N;                 // actual k and n (complex); KC/BN may pad them
+    int kpair, ypair;         // 1: k index bit 0 is A's bit 0 / n index bit 0 is C's bit 0 -> 16-byte loads / stores
     const uint32_t* tab;      // [ntab][256][2]: (A offset, C offset) of the orbit index bytes
     int ntab;
     const uint32_t* koff;     // [K]: A offset of k
@@ -174,7 +175,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
                     }
                     const float2* __restrict__ src = p.A + ra * p.a_row + aoff;
 #pragma unroll
-                    for (int kk = 0; kk < KV; kk++) v[rr * KV + kk] = __ldg(src + s_koff[kk]);
+                    if (KV >= 2 && p.kpair) {  // (kk, kk + 1) adjacent in memory: one 16-byte load
+#pragma unroll
+                        for (int kk = 0; kk < KV; kk += 2) {
+                            const float4 w = __ldg((const float4*)(src + s_koff[kk]));
+                            v[rr * KV + kk] = make_float2(w.x, w.y);
+                            v[rr * KV + kk + 1] = make_float2(w.z, w.w);
+                        }
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < KV; kk++) v[rr * KV + kk] = __ldg(src + s_koff[kk]);
+                    }
                 } else {
 #pragma unroll
                     for (int kk = 0; kk < KV; kk++) v[rr * KV + kk] = make_float2(0.f, 0.f);
@@ -325,7 +336,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
                         : "r"(taddr));
                 }
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (valid && p.mode != 2) {
+                if (valid && p.mode != 2 && p.ypair) {  // (n, n + 1) adjacent in C: one 16-byte store
+#pragma unroll
+                    for (int q = 0; q < CH / 2; q += 2) {
+                        const int n = (c0 >> 1) + q;
+                        if (n < p.N)
+                            *(float4*)(dst + s_yoff[n]) = make_float4(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1]),
+                                                                      __uint_as_float(u[2 * q + 2]), __uint_as_float(u[2 * q + 3]));
+                    }
+                } else if (valid && p.mode != 2) {
 #pragma unroll
                     for (int q = 0; q < CH / 2; q++) {
                         const int n = (c0 >> 1) + q;
