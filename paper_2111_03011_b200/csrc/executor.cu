@@ -872,33 +872,46 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                     if ((kk >> t) & 1) o += 1u << a.kA[ko[t]];
                 tabs.push_back(o);
             }
-            const size_t yt = tabs.size();
-            for (int n = 0; n < g.N; n++) {
-                uint32_t o = 0;
-                for (int u = 0; u < nb; u++)
-                    if ((n >> u) & 1) o += 1u << a.cB.dst[no[u]];
-                tabs.push_back(o);
-            }
-            const size_t gt = tabs.size();
-            for (int kk = 0; kk < g.K; kk++)
-                for (int n = 0; n < g.N; n++) {
-                    uint32_t o = 0;
-                    for (int t = 0; t < nk; t++)
-                        if ((kk >> t) & 1) o += 1u << a.kB[ko[t]];
-                    for (int u = 0; u < nb; u++)
-                        if ((n >> u) & 1) o += 1u << a.cB.src[no[u]];
-                    tabs.push_back(o);
-                }
-            fixes.push_back({P.launches.size(), 9, tb});
-            fixes.push_back({P.launches.size(), 10, kt});
-            fixes.push_back({P.launches.size(), 11, yt});
-            fixes.push_back({P.launches.size(), 12, gt});
+            // k = 32 with 128 output columns exceeds the shared-memory budget of one launch (KC = 64, BN <= 128):
+            // split the output columns into launches of 64 (each re-reads A; the columns' n index top bit differs)
+            const int nsplit = (L.g_kc == 64 && g.mode != 2 && g.N > 64) ? g.N / 64 : 1;
+            const int Np = g.N / nsplit;
             L.grid = dim3((unsigned)std::min<int64_t>(g.n_tiles, 148));
             L.block = dim3(gtc::THREADS);
             L.m = g.n_orb * a.R;
-            L.n = g.N;
+            L.n = Np;
             L.k = g.K;
             L.rows = a.R;
+            L.g_bn = 2 * std::max(8, (g.mode == 2 ? g.GM : 1) * Np);
+            L.bytes = st.bytes / nsplit;
+            L.cmac = st.cmac / nsplit;
+            for (int part = 0; part < nsplit; part++) {
+                Launch Lp = L;
+                Lp.gd.N = Np;
+                const size_t yt = tabs.size();
+                for (int n = part * Np; n < (part + 1) * Np; n++) {
+                    uint32_t o = 0;
+                    for (int u = 0; u < nb; u++)
+                        if ((n >> u) & 1) o += 1u << a.cB.dst[no[u]];
+                    tabs.push_back(o);
+                }
+                const size_t gt = tabs.size();
+                for (int kk = 0; kk < g.K; kk++)
+                    for (int n = part * Np; n < (part + 1) * Np; n++) {
+                        uint32_t o = 0;
+                        for (int t = 0; t < nk; t++)
+                            if ((kk >> t) & 1) o += 1u << a.kB[ko[t]];
+                        for (int u = 0; u < nb; u++)
+                            if ((n >> u) & 1) o += 1u << a.cB.src[no[u]];
+                        tabs.push_back(o);
+                    }
+                fixes.push_back({P.launches.size(), 9, tb});
+                fixes.push_back({P.launches.size(), 10, kt});
+                fixes.push_back({P.launches.size(), 11, yt});
+                fixes.push_back({P.launches.size(), 12, gt});
+                if (part + 1 < nsplit) P.launches.push_back(Lp);
+                else L = Lp;
+            }
         } else if (st.kind == K_APPLY) {
             const ApplyParams& a = st.ap;
             kern::ApplyDev& p = L.ap;

@@ -421,7 +421,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
                 const int nk = ap.nk, nb = ap.cB.n;
                 // measured on config 4: 16x16 gates 3.5 ms (TC) vs 5.8 ms (SIMT) on a 2^30 stem; 8x8 gates are
                 // faster on SIMT (4.7 vs 5.6 ms), so small k needs a wide output to go to the tensor cores
-                const bool fits = nk >= 3 && nk <= 5 && nb >= 1 && nb <= (nk <= 4 ? 7 : 6) && ap.cA.n <= 32 &&
+                const bool fits = nk >= 3 && nk <= 5 && nb >= 1 && nb <= 7 && ap.cA.n <= 32 &&
                                   (nk >= 4 || nb >= 4);
                 const bool big = (double)RC * std::ldexp(1.0, ap.cA.n) >= 1048576.0 && cmac >= 4.0 * 1048576.0 * 16;
                 static const bool gate_off = getenv("TNB_NO_GATE_TC") != nullptr;
@@ -452,7 +452,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
                         st.ap.gperm = BufRef{REG_MAPS, push_blob(prog.maps, perm.data(), perm.size() * 4)};
                         st.ap.gstart = BufRef{REG_MAPS, push_blob(prog.maps, gs.data(), gs.size() * 4)};
                         st.ap.gcnt = BufRef{REG_MAPS, push_blob(prog.maps, cnt.data(), cnt.size() * 4)};
-                    } else if (RB * 8 <= RC && nb <= (nk <= 4 ? 7 : 6) && (nk >= 4 || nb >= 4)) {
+                    } else if (RB * 8 <= RC && nb <= 7 && (nk >= 4 || nb >= 4)) {
                         std::vector<int32_t> perm(RC);
                         for (int64_t r = 0; r < RC; r++) perm[r] = (int32_t)r;
                         std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) { return mb[x] < mb[y]; });

@@ -109,7 +109,7 @@ inline StepCost step_cost(int a, int b, int c, int u, double rA, double rB, doub
                    const int dsmall = a_small ? a : b, dbig = a_small ? b : a;
                    const double rbig = a_small ? rB : rA;
                    const int fb = dsmall - kk, fa = dbig - kk;
-                   return kk >= 3 && kk <= 5 && fb >= 1 && fb <= (kk <= 4 ? 7 : 6) && fa <= 32 && (kk >= 4 || fb >= 4) &&
+                   return kk >= 3 && kk <= 5 && fb >= 1 && fb <= 7 && fa <= 32 && (kk >= 4 || fb >= 4) &&
                           rbig * std::ldexp(1.0, fa) >= 1048576.0 && s.cmac >= 4.0 * 1048576.0 * 16;
                }()) {
         s.time = std::max(s.cmac / C_TC, s.bytes / BW) + T_LAUNCH;
