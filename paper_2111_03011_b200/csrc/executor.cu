@@ -864,7 +864,7 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
             for (int u = 0; u < nb; u++)
                 if (a.cB.dst[u] == 0) std::swap(no[0], no[u]);
             g.kpair = (nk >= 1 && a.kA[ko[0]] == 0) ? 1 : 0;
-            g.ypair = (nb >= 1 && a.cB.dst[no[0]] == 0 && g.mode != 2) ? 1 : 0;
+            g.ypair = (nb >= 1 && a.cB.dst[no[0]] == 0) ? 1 : 0;
             const size_t kt = tabs.size();
             for (int kk = 0; kk < g.K; kk++) {
                 uint32_t o = 0;

@@ -350,6 +350,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
                         const int n = (c0 >> 1) + q;
                         if (n < p.N) dst[s_yoff[n]] = make_float2(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1]));
                     }
+                } else if (valid && p.ypair) {  // mode 2, (n, n + 1) of one member adjacent in C
+#pragma unroll
+                    for (int q = 0; q < CH / 2; q += 2) {
+                        const int ne = (c0 >> 1) + q, i = ne >> lgN, n = ne & (p.N - 1);
+                        if (i < members)
+                            *(float4*)(p.C + s_mrow[quarter][i] + coff + s_yoff[n]) =
+                                make_float4(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1]),
+                                            __uint_as_float(u[2 * q + 2]), __uint_as_float(u[2 * q + 3]));
+                    }
                 } else if (valid) {
 #pragma unroll
                     for (int q = 0; q < CH / 2; q++) {
