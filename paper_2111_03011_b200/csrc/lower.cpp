@@ -287,8 +287,11 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             const double cm = (double)RC * std::ldexp(1.0, (int)(fa + fb + K.size()));
             const int64_t RA = (int64_t)A->rows.size();
             // (short k, <= 32, goes to the gate kernel's modes 1 / 2 below, which read A once without a pre-pass)
+            // (either operand may be the gate kernel's stem: the one with the longer rows, whose free legs must
+            // fill whole tiles)
+            const int64_t fbig = per_row(*A) >= per_row(*B) ? fa : fb;
             grouped = K.size() >= 4 && fa >= 5 && cm >= 16.0 * 1024 * 1024 &&
-                      (RC >= 16 * RA || (fa >= 7 && RC >= 2 * RA)) && !(K.size() <= 5 && fa >= 7);
+                      (RC >= 16 * RA || (fa >= 7 && RC >= 2 * RA)) && !(K.size() <= 5 && fbig >= 7);
             if (!grouped && per_row(*B) > per_row(*A)) std::swap(A, B);  // SIMT: stream the larger rows
             use_gemm = grouped;
         } else {
