@@ -180,6 +180,20 @@ def workload_config(cfg, slices_per_step) -> dict:
             "slices_per_step": slices_per_step, "max_tensor_size": 1 << cfg.log2_tmax}
 
 
+def fidelity_target_time(r, info, world, F=0.002):
+    """Time to the M amplitudes of an approximate state of fidelity F (the sampling task's target: Google's
+    XEB 0.002, PAPER.md L38 / L215): summing a fraction f of the global slices gives fidelity ~ f (the sliced
+    paths are orthogonal and contribute equally, PAPER.md L77 / L152 / L248; checked for prefixes by
+    tests/test_gpu_fidelity.py), so f = F slices are needed -- the partial-path sum the paper makes with its K = 8
+    broken edges.  Computed from the MEASURED slices/s (blocks of consecutive slice ids, as timed), not
+    extrapolated from a model."""
+    nS = 1 << info["s"]
+    need = max(1, int(-(-F * nS // 1)))
+    return {"fidelity": F, "global_slices": need, "of": nS, "seconds": need / r["value"],
+            "cmac": info["total_cmac"] * need / nS, "n_gpus": world,
+            "note": "measured slices/s x the slice count for fidelity F (fidelity ~ summed fraction)"}
+
+
 def plan_ss(T, cfg, plan_path, log2_tmax):
     circ = cfg.circuit()
     n = circ["n"]
@@ -509,6 +523,7 @@ def main():
             "plan_total_cmac": info["total_cmac"],
             "time_to_M_amplitudes_s": main_r["extrap"]["seconds"],
             "time_to_M_amplitudes": main_r["extrap"],
+            "time_to_M_amplitudes_at_F": fidelity_target_time(main_r, info, world),
             "e2e": main_r["e2e"],
             "roofline": main_r["roofline"],
             "roofline_tensor": main_r["roofline_tensor"],

@@ -110,7 +110,9 @@ typedef struct {
                                     on the other qubit is projected onto the dominant singular vector
                                     of the pinned gate, i.e. onto |v> in G's input basis with v the
                                     sliced wire's value (cutting that companion edge too); fidelity
-                                    factor (1 + sin^2 theta)/2 each                      */
+                                    factor (1 + sin^2 theta)/2 each.  Flat plans and loop
+                                    programs (the interface's companion edges); with
+                                    plan_path it must equal the plan file's "companions" flag       */
     int32_t method;              /* 0 auto (loop program above 160 tensors), 1 flat slicing (every
                                     sliced wire is a slice-id bit), 2 loop program: a stem sweep with
                                     local slices summed inside the program and checkpointed segments
@@ -140,7 +142,8 @@ typedef struct {
     double invariant_cmac;       /* tn_contract, before the slices (their CMACs)              */
     int32_t n_companions;        /* companion edges cut (tn_slicing.companions)               */
     const int32_t* companion_wires; /* 3*n ints: (q, k, b): Pi_v on wire (q, k) -- right before
-                                    the fSim, after its single-qubit gates -- with v = slice bit b
+                                    the fSim, after its single-qubit gates -- with v = the value of
+                                    sliced wire b, counted in sliced_wires and then local_wires
                                     (owned by ctx)                                             */
     double companion_fidelity;   /* prod (1 + sin^2 theta_i)/2 over the companions   */
     int32_t s_local;             /* loop program: local sliced wires, summed inside tn_contract    */

@@ -175,14 +175,16 @@ tn_status tn_plan(tn_ctx* ctx, const tn_slicing* slicing, int64_t max_tensor_siz
     tnb::Plan plan;
     std::string e;
     if (slicing && slicing->plan_path) {
-        if (slicing->companions) return fail(ctx, TN_EINVAL, "plan import does not support companion edges");
         e = tnb::load_plan(ctx->net, ctx->leaves, slicing->plan_path, plan);
         if (!e.empty()) return fail(ctx, TN_EINVAL, e);
+        if ((slicing->companions != 0) != plan.companions)
+            return fail(ctx, TN_EINVAL, "tn_slicing.companions differs from the plan file's companions flag");
     } else {
         e = tnb::find_plan(ctx->net, ctx->leaves, ctx->req, opt, plan);
         if (!e.empty()) return fail(ctx, TN_EINFEASIBLE, e);
     }
     if (slicing && slicing->companions) {
+        plan.companions = true;
         // the companion edges change the network (exact basis changes) and the leaves: plan on a copy
         tnb::Network net2 = ctx->net;
         tnb::add_companions(net2, plan);
@@ -231,10 +233,14 @@ tn_status tn_plan(tn_ctx* ctx, const tn_slicing* slicing, int64_t max_tensor_siz
     I.invariant_cmac = ctx->prog.pre_cmac;
     ctx->companion_wires.clear();
     I.companion_fidelity = 1.0;
+    // a companion's partner index counts in sliced_wires, then local_wires (loop programs)
+    std::vector<int> pub(s_all, 0);
+    for (int i = 0, ng = 0, nl = 0; i < s_all; i++)
+        pub[i] = (plan.segs.empty() || plan.is_global[i]) ? ng++ : s_glob + nl++;
     for (size_t t = 0; t < plan.tied.size(); t++) {
         ctx->companion_wires.push_back(plan.tied_wire[t].first);
         ctx->companion_wires.push_back(plan.tied_wire[t].second);
-        ctx->companion_wires.push_back(plan.tied[t].second);
+        ctx->companion_wires.push_back(pub[plan.tied[t].second]);
         I.companion_fidelity *= plan.tied_factor[t];
     }
     I.n_companions = (int32_t)plan.tied.size();

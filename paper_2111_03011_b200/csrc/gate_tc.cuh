@@ -153,6 +153,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
         // ------------------------------------------------------------ producers: gather + split + swizzle
         const int g = threadIdx.x / PG, tid = threadIdx.x % PG;
         int it = g;
+        // modes 1, 2: the A row of the last unit seen per row slot (consecutive tiles mostly stay in one output
+        // row, so the dependent perm / ma loads are paid once per row, not once per tile)
+        int64_t last_u[RPT], last_ra[RPT];
+#pragma unroll
+        for (int rr = 0; rr < RPT; rr++) last_u[rr] = -1, last_ra[rr] = 0;
         for (int64_t t = tb + g; t < te; t += NG, it += NG) {
             const int s = it % STAGES;
             const uint32_t ph = (it / STAGES) & 1;
@@ -170,8 +175,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
                     for (int b = 0; b < p.ntab; b++) aoff += s_tab[(b * 256 + (int)((o >> (8 * b)) & 255)) * 2];
                     int64_t ra = u;
                     if (p.mode != 2) {
-                        const int64_t r = out_row(u);
-                        ra = p.ma ? (int64_t)p.ma[r] : r;
+                        if (u != last_u[rr]) {
+                            const int64_t r = out_row(u);
+                            last_ra[rr] = p.ma ? (int64_t)p.ma[r] : r;
+                            last_u[rr] = u;
+                        }
+                        ra = last_ra[rr];
                     }
                     const float2* __restrict__ src = p.A + ra * p.a_row + aoff;
 #pragma unroll
@@ -215,13 +224,18 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
         // ------------------------------------------------------------ MMA issuer (+ gate loads)
         constexpr uint32_t idesc = tc::idesc_tf32(ROWS, BN);
         const uint32_t bth = tc::smem_u32(bt), btl = bth + CF::NKB * CF::BTILE;
-        int64_t cur = -1;
+        int64_t cur = -1, last_u0 = -1, last_gid = 0;
         uint32_t gph = 0;
         int it = 0;
         for (int64_t t = tb; t < te; t++, it++) {
-            // the tile's gate: mode 0 one gate; mode 1 the G row of the tile's output row; mode 2 the tile's A row
+            // the tile's gate: mode 0 one gate; mode 1 the G row of the tile's output row (looked up once per
+            // output row: the dependent perm / mb loads would stall the issuer every tile); mode 2 the tile's A row
             const int64_t u0 = (t * ROWS) >> p.log2_orb;
-            const int64_t gid = p.mode == 0 ? 0 : (p.mode == 1 ? (int64_t)p.mb[out_row(u0)] : u0);
+            if (p.mode == 1 && u0 != last_u0) {
+                last_gid = (int64_t)p.mb[out_row(u0)];
+                last_u0 = u0;
+            }
+            const int64_t gid = p.mode == 0 ? 0 : (p.mode == 1 ? last_gid : u0);
             if (gid != cur) {
                 if (cur >= 0) {  // drain: every MMA that reads the resident gate has completed
                     if (lane == 0) tc::mma_commit(gfree);
@@ -286,31 +300,42 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
         const int row = quarter * 32 + lane;
         constexpr int CH = BN < 32 ? BN : 32;  // TMEM columns per load
         int it = 0;
+        // the output row of the last unit (mode 1) and the member table of the last A row (mode 2) are kept across
+        // tiles: the dependent index loads would otherwise sit in every tile's epilogue (~1-2 us, about one
+        // tile's HBM time), and are looked up before the accumulator wait so their latency hides behind it
+        int64_t last_uu = -1, last_crow = 0, last_u0 = -1;
+        int members = 0;
+        const int lgN = 31 - __clz(p.N);
         for (int64_t t = tb; t < te; t++, it++) {
             const int buf = it & 1;
             const uint32_t tph = (it >> 1) & 1;
+            const int64_t x = t * ROWS + row;
+            if (p.mode == 2) {
+                // a tile lies in one A row, so the whole warp shares the members' output row offsets
+                const int64_t u0 = (t * ROWS) >> p.log2_orb;
+                if (u0 != last_u0) {
+                    members = p.gcnt[u0];
+                    __syncwarp();
+                    if (lane < members) s_mrow[quarter][lane] = (int64_t)p.perm[p.gstart[u0] + lane] * p.c_row;
+                    __syncwarp();
+                    last_u0 = u0;
+                }
+            } else if (x < total) {
+                const int64_t u1 = x >> p.log2_orb;
+                if (u1 != last_uu) {
+                    last_crow = out_row(u1) * p.c_row;
+                    last_uu = u1;
+                }
+            }
             tc::mbar_wait(&tfull[buf], tph);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int64_t x = t * ROWS + row;
             const bool valid = x < total;
             uint32_t coff = 0;
-            int64_t uu = 0;
             float2* dst = nullptr;
             if (valid) {
-                uu = x >> p.log2_orb;
                 const int64_t o = x & (p.n_orb - 1);
                 for (int b = 0; b < p.ntab; b++) coff += s_tab[(b * 256 + (int)((o >> (8 * b)) & 255)) * 2 + 1];
-                if (p.mode != 2) dst = p.C + out_row(uu) * p.c_row + coff;
-            }
-            int members = 0, lgN = 0;
-            if (p.mode == 2) {
-                // the members' output row offsets, one warp-level table per tile (a tile lies in one A row, so the
-                // whole warp shares them): one LDS per output instead of dependent global loads
-                const int64_t u0 = (t * ROWS) >> p.log2_orb;
-                members = p.gcnt[u0];
-                if (lane < members) s_mrow[quarter][lane] = (int64_t)p.perm[p.gstart[u0] + lane] * p.c_row;
-                __syncwarp();
-                lgN = 31 - __clz(p.N);
+                if (p.mode != 2) dst = p.C + last_crow + coff;
             }
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += CH) {

@@ -11,7 +11,8 @@
 //    "n_global": g,                                        // -1: flat slicing (all bits are slice ids)
 //    "global":  [1 if sliced[i] is a slice-id bit, ...],
 //    "step_seg": [segment of step p, ...],
-//    "segs":    [[D, Sum, E], ...]}                        // tau-bit masks (decimal)
+//    "segs":    [[D, Sum, E], ...],                        // tau-bit masks (decimal)
+//    "companions": 0 | 1}                                  // 1: tie the sliced wires' companion edges
 #include <cctype>
 #include <cstdlib>
 #include <fstream>
@@ -140,7 +141,7 @@ std::string save_plan(const Network& net, const std::vector<Leaf>& leaves, const
     f << "],\n \"segs\": [";
     for (size_t j = 0; j < plan.segs.size(); j++)
         f << (j ? "," : "") << "[" << plan.segs[j].D << "," << plan.segs[j].Sum << "," << plan.segs[j].E << "]";
-    f << "]}\n";
+    f << "],\n \"companions\": " << (plan.companions ? 1 : 0) << "}\n";
     return f ? "" : "write failed: " + path;
 }
 
@@ -233,6 +234,8 @@ std::string load_plan(const Network& net, const std::vector<Leaf>& leaves, const
         }
         if (summed != local) return "plan file: the summed bits must be exactly the local bits";
     }
+    const JV* jc = get("companions");
+    pl.companions = jc && jc->i64() != 0;
     plan = pl;
     return "";
 }

@@ -714,7 +714,9 @@ struct Sweep {
     std::vector<std::vector<std::pair<int, int>>> nbr;  // per leaf: (other endpoint leaf, edge) per internal leg
     std::vector<int> deg;                // dense legs per leaf (internal + open)
     std::vector<uint64_t> q;
-    std::vector<char> sliced;            // per edge
+    std::vector<char> sliced;            // per edge: 1 = sliced (own loop bit), 2 = companion tied to a sliced edge
+    std::vector<int> tie;                // per edge: the sliced partner of a tied companion edge, else -1
+    const std::vector<std::pair<int, int>>* comps = nullptr;  // (sliced edge, companion edge), add_companions order
     double tmax = 1e300;                 // soft bound on every stem size (per slice)
     int local = 1;                       // sum each sliced edge right after the step that closes it
     RowModel* rm = nullptr;
@@ -740,6 +742,20 @@ inline double sweep_cost(double rows, int uni, int b, int sk, double tmax) {
 }
 
 // recompute positions lo..hi (inclusive) from the state at lo-1; returns the new sum of C over lo..hi
+// companion edges ("rank one approximation to companion edges"): every sliced edge's companion
+// that add_companions would cut is tied to the partner's bit; the tie removes its dense leg but adds no loop
+void sweep_retie(Sweep& S) {
+    for (size_t e = 0; e < S.sliced.size(); e++)
+        if (S.sliced[e] == 2) S.sliced[e] = 0;
+    std::fill(S.tie.begin(), S.tie.end(), -1);
+    if (!S.comps) return;
+    for (const auto& pc : *S.comps)
+        if (S.sliced[pc.first] == 1 && S.sliced[pc.second] == 0) {
+            S.sliced[pc.second] = 2;
+            S.tie[pc.second] = pc.first;
+        }
+}
+
 inline double sweep_range(const Sweep& S, SweepState& st, int lo, int hi) {
     int b = lo > 0 ? st.B[lo - 1] : 0;
     int sk = lo > 0 ? st.Sk[lo - 1] : 0;
@@ -751,6 +767,7 @@ inline double sweep_range(const Sweep& S, SweepState& st, int lo, int hi) {
         for (const auto& ue : S.nbr[v]) {
             if (S.sliced[ue.second]) {
                 sl_deg++;
+                if (S.sliced[ue.second] == 2) continue;
                 if (st.pos[ue.first] > k) sl_new++;
                 else sl_close++;
             } else {
@@ -883,9 +900,17 @@ StemEvents stem_events(const Sweep& S, const SweepState& st, const Network& net,
         ev.size[k] = r * std::ldexp(1.0, b);
     }
     for (int e = 0; e < (int)S.sliced.size(); e++) {
-        if (!S.sliced[e]) continue;
-        const int pa = st.pos[slot_of_tensor[net.edges[e].t0]], pb = st.pos[slot_of_tensor[net.edges[e].t1]];
-        ev.ab.push_back({std::min(pa, pb), std::max(pa, pb)});
+        if (S.sliced[e] != 1) continue;
+        int lo = std::min(st.pos[slot_of_tensor[net.edges[e].t0]], st.pos[slot_of_tensor[net.edges[e].t1]]);
+        int hi = std::max(st.pos[slot_of_tensor[net.edges[e].t0]], st.pos[slot_of_tensor[net.edges[e].t1]]);
+        // a tied companion reads the same bit: the loop spans its endpoints too
+        for (int c = 0; c < (int)S.tie.size(); c++)
+            if (S.tie[c] == e)
+                for (int t : {net.edges[c].t0, net.edges[c].t1}) {
+                    lo = std::min(lo, st.pos[slot_of_tensor[t]]);
+                    hi = std::max(hi, st.pos[slot_of_tensor[t]]);
+                }
+        ev.ab.push_back({lo, hi});
         ev.edge.push_back(e);
     }
     return ev;
@@ -1175,6 +1200,10 @@ std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         hp.push_back({ev.cmac, std::move(t)});
     }
     std::sort(hp.begin(), hp.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    if (verbose)
+        for (int k = 0; k < std::min<int>(5, (int)hp.size()); k++)
+            fprintf(stderr, "[plan] bisection tree %d: unsliced %.3e CMAC, peak 2^%.1f (%zu trees, %.1f s)\n", k,
+                    hp[k].first, std::log2(eval_tree(hp[k].second, none).peak), hp.size(), elapsed());
     // ---------------- 2. sweeps
     Sweep S;
     S.NL = NL;
@@ -1183,6 +1212,8 @@ std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     S.deg.resize(NL);
     S.q.resize(NL);
     S.sliced.assign(net.edges.size(), 0);
+    S.tie.assign(net.edges.size(), -1);
+    if (!opt.companions.empty()) S.comps = &opt.companions;
     for (int i = 0; i < NL; i++) {
         S.deg[i] = (int)leaves[i].legs.size();
         S.q[i] = leaves[i].qmask;
@@ -1195,7 +1226,8 @@ std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     // sweep objective: TNB_SWEEP_LOCAL=0 anneals under prefix caching only (every touched sliced edge stays open),
     // which is what the laminar loop nest mostly reduces to when the stem keeps its sliced legs to the end
     if (getenv("TNB_SWEEP_LOCAL")) S.local = atoi(getenv("TNB_SWEEP_LOCAL"));
-    const int64_t iters = opt.sweep_iters > 0 ? opt.sweep_iters : std::max<int64_t>(20000, (int64_t)NL * 4000);
+    int64_t iters = opt.sweep_iters > 0 ? opt.sweep_iters : std::max<int64_t>(20000, (int64_t)NL * 4000);
+    if (getenv("TNB_SWEEP_ITERS")) iters = atoll(getenv("TNB_SWEEP_ITERS"));
     const double pbudget = opt.persist_budget > 0 ? opt.persist_budget : 8.0 * opt.max_elems;
     auto peak_of = [&](const SweepState& x) {
         double pk = 0;
@@ -1211,6 +1243,7 @@ std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     for (int k = 0; k < (int)hp.size() && (k < 2 || elapsed() < budget); k++) {
         std::fill(S.sliced.begin(), S.sliced.end(), 0);
         for (int e : opt.forced) S.sliced[e] = 1;
+        sweep_retie(S);
         S.tmax = 1e300;
         SweepState st;
         sweep_init(S, st, leaf_order(hp[k].second));
@@ -1233,13 +1266,17 @@ std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             SweepState tmp = st;
             for (int e : internal) {
                 if (!cand[e]) continue;
+                const char was = S.sliced[e];
                 S.sliced[e] = 1;
+                if (S.comps) sweep_retie(S);
                 const double tt = sweep_range(S, tmp, 0, NL - 1);
-                S.sliced[e] = 0;
+                S.sliced[e] = was;
+                if (S.comps) sweep_retie(S);
                 if (tt < bt) { bt = tt; be = e; }
             }
             if (be < 0) { ok = false; break; }
             S.sliced[be] = 1;
+            sweep_retie(S);
             st.total = sweep_range(S, st, 0, NL - 1);
             sweep_anneal(S, st, rng, iters / 8, 0.2, 0.01);
         }
@@ -1290,7 +1327,7 @@ std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     // one tensor-core-sized step; it never moves work across a checkpoint
     Bits Sall;
     for (int e = 0; e < (int)best_sliced.size(); e++)
-        if (best_sliced[e]) Sall.set(e);
+        if (best_sliced[e] == 1) Sall.set(e);
     const double t_before = eval_tree(t, Sall).time;
     {
         Ctx cx{&rm, Sall, opt.max_elems};
@@ -1346,9 +1383,11 @@ std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         fprintf(stderr, "[plan] loop program: %d global + %d local bits, %d segments, total %.3e CMAC, persist 2^%.1f\n",
                 pl.n_global, ns - pl.n_global, J, pl.total_cmac, std::log2(std::max(1.0, pl.persist_elems)));
         for (int j = 0; j < J; j++)
-            fprintf(stderr, "[plan]   seg %d: steps ..%d  |D| %d  |Sum| %d  |E| %d\n", j, cp[j],
-                    __builtin_popcountll(pl.segs[j].D), __builtin_popcountll(pl.segs[j].Sum),
-                    __builtin_popcountll(pl.segs[j].E));
+            fprintf(stderr, "[plan]   seg %d: steps ..%d  |D| %d  |Sum| %d  |E| %d  run %.3e CMAC x 2^%d = %.3e  stem 2^%.1f rows 2^%.1f\n",
+                    j, cp[j], __builtin_popcountll(pl.segs[j].D), __builtin_popcountll(pl.segs[j].Sum),
+                    __builtin_popcountll(pl.segs[j].E), LN.segc[j], __builtin_popcountll(pl.segs[j].D),
+                    LN.segc[j] * std::ldexp(1.0, __builtin_popcountll(pl.segs[j].D)), std::log2(best_ev.size[cp[j]]),
+                    std::log2(rm.estimate(best_st.Q[cp[j]])));
     }
     out = pl;
     return "";
@@ -1394,7 +1433,6 @@ std::string find_plan(const Network& net, const std::vector<Leaf>& leaves, const
 
     const int method = opt.method != 0 ? opt.method : (NL > 160 ? 2 : 1);
     if (method == 2) {
-        if (!opt.companions.empty()) return "companion edges are not supported by the loop-program planner";
         return sweep_plan(net, leaves, req, opt, internal, slot_of_tensor, rm, rng, budget, out);
     }
     // ---------------- 1. greedy trees; keep the best few by unsliced modelled time

@@ -110,6 +110,7 @@ struct Plan {
     // bits restricted to the caller's slice ids) and runs a segment when all its Sum bits are 1 and its D bits
     // differ from its previous run; E = local bits summed (accumulated) at the end of the segment.
     int n_global = -1;
+    bool companions = false;  // plan file flag: the companion edges of the sliced wires are tied (add_companions)
     std::vector<char> is_global;   // loop program: per entry of `sliced`, 1 = a slice-id bit (any position)
     std::vector<int> step_seg;
     struct Seg {

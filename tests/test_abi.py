@@ -316,3 +316,28 @@ def test_companion_plan_report(T):
                     break
         want *= (1 + math.sin(theta) ** 2) / 2
     assert abs(info["companion_fidelity"] - want) < 1e-12
+
+
+def test_loop_program_companions_and_plan_file_flag(T, tmp_path):
+    """Loop programs accept companion edges: each companion is the oracle's companion of its partner,
+    indexed in sliced_wires + local_wires; the plan file records the flag, and importing it with a different
+    tn_slicing.companions is refused (the tied edges change the lowered network)."""
+    from oracle import sv
+    c = configs.get(2)
+    circ = c.circuit()
+    n = circ["n"]
+    bits = c.bitstrings(n)
+    ss = T.SparseState(circ, bits, c.open_mask(n))
+    info = ss.plan(1 << 12, n_sliced=2, method=2, max_segments=8, seed=1, time_budget_s=5.0, companions=True)
+    W = info["sliced_wires"] + info["local_wires"]
+    assert info["companions"] and info["s_local"] >= 1
+    for (q, k, i) in info["companions"]:
+        assert sv.companion_of(circ, W[i]) == (q, k)
+    p = str(tmp_path / "plan.json")
+    ss.save_plan(p)
+    ss2 = T.SparseState(circ, bits, c.open_mask(n))
+    with pytest.raises(T.TnError) as e:
+        ss2.plan(1 << 12, plan_path=p)
+    assert e.value.status == T.TN_EINVAL
+    info2 = ss2.plan(1 << 12, plan_path=p, companions=True)
+    assert info2["companions"] == info["companions"] and info2["total_cmac"] == info["total_cmac"]

@@ -104,3 +104,26 @@ def test_loop_program_24q_random_circuit(T, oracle_built):
     amps = ss.contract(range(1 << info["s"])).cpu().numpy()
     want, _ = sv.amplitudes(circ, bits)
     assert_amps_close(amps, want)
+
+
+def test_loop_program_with_companions(T, oracle_built, cfg2):
+    """Loop program with companion-edge truncation ("rank one approximation to companion
+    edges" of the interface): every companion is Pi_v on the oracle's companion wire with v the value of its
+    partner (global or local), so the oracle enumerates the local wires too and sums their values itself
+    (Sigma_v Pi_v x Pi_v != I on a tied pair)."""
+    from oracle import sv
+    c, circ, bits, om = cfg2
+    ss = T.SparseState(circ, bits, om)
+    info = ss.plan(1 << 12, n_sliced=2, method=2, max_segments=8, seed=1, time_budget_s=5.0, companions=True)
+    comps = info["companions"]
+    assert len(comps) >= 1 and info["s_local"] >= 1, info
+    W = info["sliced_wires"] + info["local_wires"]
+    for (q, k, i) in comps:
+        assert sv.companion_of(circ, W[i]) == (q, k)
+    ss.bind(0, pipelines=4)
+    s, sl = info["s"], info["s_local"]
+    for glob in (range(1 << s), [1]):
+        ids = [(g << sl) | lam for g in glob for lam in range(1 << sl)]
+        want = sv.sliced_amplitudes(circ, bits, W, ids, companions=comps)
+        assert_amps_close(ss.contract(glob).cpu().numpy(), want)
+    assert 0.9 < info["companion_fidelity"] <= 1.0
