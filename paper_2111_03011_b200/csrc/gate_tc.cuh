@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
     __shared__ uint32_t s_tab[4 * 256 * 2];
     __shared__ uint32_t s_koff[32];
     __shared__ uint32_t s_yoff[128];
-    __shared__ int64_t s_mrow[4][32];  // mode 2: output row offsets of the tile's members, per epilogue warp
+    __shared__ int64_t s_cofs[4][128];  // mode 2: C offset of gate column (member i, n), per epilogue warp
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < p.ntab * 512; i += THREADS) s_tab[i] = p.tab[i];
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
         // tiles: the dependent index loads would otherwise sit in every tile's epilogue (~1-2 us, about one
         // tile's HBM time), and are looked up before the accumulator wait so their latency hides behind it
         int64_t last_uu = -1, last_crow = 0, last_u0 = -1;
-        int members = 0;
+        int nvalid = 0;  // mode 2: valid gate columns (members x N) of the current A row
         const int lgN = 31 - __clz(p.N);
         for (int64_t t = tb; t < te; t++, it++) {
             const int buf = it & 1;
@@ -314,9 +314,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
                 // a tile lies in one A row, so the whole warp shares the members' output row offsets
                 const int64_t u0 = (t * ROWS) >> p.log2_orb;
                 if (u0 != last_u0) {
-                    members = p.gcnt[u0];
+                    // one C offset per gate column (member row + output legs): each store is then one LDS + add,
+                    // like mode 0 (the per-store member lookup made the epilogue the bottleneck: ncu, 2.9 TB/s)
+                    const int members = p.gcnt[u0];
+                    nvalid = members * p.N;
                     __syncwarp();
-                    if (lane < members) s_mrow[quarter][lane] = (int64_t)p.perm[p.gstart[u0] + lane] * p.c_row;
+                    for (int e = lane; e < nvalid; e += 32)
+                        s_cofs[quarter][e] = (int64_t)p.perm[p.gstart[u0] + (e >> lgN)] * p.c_row + s_yoff[e & (p.N - 1)];
                     __syncwarp();
                     last_u0 = u0;
                 }
@@ -376,21 +380,22 @@ __global__ void __launch_bounds__(THREADS, 1) k_gate_tc(const GateDev p) {
                         if (n < p.N) dst[s_yoff[n]] = make_float2(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1]));
                     }
                 } else if (valid && p.ypair) {  // mode 2, (n, n + 1) of one member adjacent in C
+                    float2* base = p.C + coff;
 #pragma unroll
                     for (int q = 0; q < CH / 2; q += 2) {
-                        const int ne = (c0 >> 1) + q, i = ne >> lgN, n = ne & (p.N - 1);
-                        if (i < members)
-                            *(float4*)(p.C + s_mrow[quarter][i] + coff + s_yoff[n]) =
+                        const int ne = (c0 >> 1) + q;
+                        if (ne < nvalid)
+                            *(float4*)(base + s_cofs[quarter][ne]) =
                                 make_float4(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1]),
                                             __uint_as_float(u[2 * q + 2]), __uint_as_float(u[2 * q + 3]));
                     }
                 } else if (valid) {
+                    float2* base = p.C + coff;
 #pragma unroll
                     for (int q = 0; q < CH / 2; q++) {
-                        const int ne = (c0 >> 1) + q, i = ne >> lgN, n = ne & (p.N - 1);
-                        if (i < members)
-                            p.C[s_mrow[quarter][i] + coff + s_yoff[n]] =
-                                make_float2(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1]));
+                        const int ne = (c0 >> 1) + q;
+                        if (ne < nvalid)
+                            base[s_cofs[quarter][ne]] = make_float2(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1]));
                     }
                 }
             }

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <map>
 #include <sstream>
+#include <string>
 
 #include "tnb.h"
 
@@ -346,16 +347,26 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
         const int64_t sizeB = (int64_t)B->rows.size() << B->legs.size();
 
         if (!use_gemm) {
-            // C legs: A's layout with the K legs replaced by the B-free legs (extra ones on top)
-            size_t nfb = fb.size(), used = 0;
-            size_t extra = nfb > K.size() ? nfb - K.size() : 0;
-            for (size_t t = 0; t < extra; t++) Cn.legs.push_back(fb[used++]);
-            for (int e : A->legs) {
-                if (has(K, e)) {
-                    if (used < nfb) Cn.legs.push_back(fb[used++]);
-                } else {
-                    Cn.legs.push_back(e);
+            // C legs.  Default: A's free legs keep their relative order in the low bits and the B-free legs go on
+            // top, so that consecutive orbits (A's low free bits) are consecutive in C (coalesced stores) and the
+            // new legs, usually contracted soon after, are high bits of the next step's A (coalesced gathers).
+            // TNB_C_LAYOUT=inplace: A's layout with the K legs replaced by the B-free legs (extra ones on top).
+            static const bool inplace = getenv("TNB_C_LAYOUT") && std::string(getenv("TNB_C_LAYOUT")) == "inplace";
+            if (inplace) {
+                size_t nfb = fb.size(), used = 0;
+                size_t extra = nfb > K.size() ? nfb - K.size() : 0;
+                for (size_t t = 0; t < extra; t++) Cn.legs.push_back(fb[used++]);
+                for (int e : A->legs) {
+                    if (has(K, e)) {
+                        if (used < nfb) Cn.legs.push_back(fb[used++]);
+                    } else {
+                        Cn.legs.push_back(e);
+                    }
                 }
+            } else {
+                for (int e : fb) Cn.legs.push_back(e);
+                for (int e : A->legs)
+                    if (!has(K, e)) Cn.legs.push_back(e);
             }
             Step st;
             st.kind = K_APPLY;
@@ -424,9 +435,14 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
                 const int nk = ap.nk, nb = ap.cB.n;
                 // measured on config 4: 16x16 gates 3.5 ms (TC) vs 5.8 ms (SIMT) on a 2^30 stem; 8x8 gates are
                 // faster on SIMT (4.7 vs 5.6 ms), so small k needs a wide output to go to the tensor cores
+                // TNB_GATE_ANY=1 (test hook): every structurally eligible step goes to the gate kernel, whatever its
+                // size, so that small networks exercise all three modes against the oracle
+                const char* gany_env = getenv("TNB_GATE_ANY");
+                const bool gany = gany_env && atoi(gany_env) != 0;
                 const bool fits = nk >= 3 && nk <= 5 && nb >= 1 && nb <= 7 && ap.cA.n <= 32 &&
-                                  (nk >= 4 || nb >= 4);
-                const bool big = (double)RC * std::ldexp(1.0, ap.cA.n) >= 1048576.0 && cmac >= 4.0 * 1048576.0 * 16;
+                                  (gany || nk >= 4 || nb >= 4);
+                const bool big = gany ||
+                                 ((double)RC * std::ldexp(1.0, ap.cA.n) >= 1048576.0 && cmac >= 4.0 * 1048576.0 * 16);
                 static const bool gate_off = getenv("TNB_NO_GATE_TC") != nullptr;
                 if (!gate_off && fits && big && B->qmask == 0 && !mbRef.region) st.kind = K_GATE;
                 // gather-contract (both operands carry rows) on the gate kernel: A's orbits fill whole tiles
@@ -443,7 +459,11 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
                     while (gm < gmax) gm *= 2;
                     const int ncols2 = gm << nb;  // complex gate columns in mode 2
                     const int cap2 = nk <= 4 ? 128 : 64;
-                    if (RC >= 2 * RA && gm <= 16 && ncols2 <= cap2 && (nk >= 4 || ncols2 >= 16 || RC >= 3 * RA)) {
+                    // mode 2 also when fewer output rows share an A row (RC >= 1.25 RA) if an A row spans >= 16
+                    // tiles: mode 1 would read A once per output row (config 4 step 198: 16.8 GB of DRAM traffic
+                    // for 10.8 GB of algorithmic bytes), mode 2 pays a gate reload per A row instead
+                    const bool share = RC >= 2 * RA || (4 * RC >= 5 * RA && ap.cA.n >= 11);
+                    if (share && gm <= 16 && ncols2 <= cap2 && (gany || nk >= 4 || ncols2 >= 16 || RC >= 3 * RA)) {
                         std::vector<int32_t> perm(RC), gs(RA, 0);
                         for (int64_t r = 0; r < RC; r++) perm[r] = (int32_t)r;
                         std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) { return ma[x] < ma[y]; });
@@ -455,7 +475,7 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
                         st.ap.gperm = BufRef{REG_MAPS, push_blob(prog.maps, perm.data(), perm.size() * 4)};
                         st.ap.gstart = BufRef{REG_MAPS, push_blob(prog.maps, gs.data(), gs.size() * 4)};
                         st.ap.gcnt = BufRef{REG_MAPS, push_blob(prog.maps, cnt.data(), cnt.size() * 4)};
-                    } else if (RB * 8 <= RC && nb <= 7 && (nk >= 4 || nb >= 4)) {
+                    } else if (nb <= 7 && (gany || (RB * 8 <= RC && (nk >= 4 || nb >= 4)))) {
                         std::vector<int32_t> perm(RC);
                         for (int64_t r = 0; r < RC; r++) perm[r] = (int32_t)r;
                         std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) { return mb[x] < mb[y]; });

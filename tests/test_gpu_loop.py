@@ -127,3 +127,30 @@ def test_loop_program_with_companions(T, oracle_built, cfg2):
         want = sv.sliced_amplitudes(circ, bits, W, ids, companions=comps)
         assert_amps_close(ss.contract(glob).cpu().numpy(), want)
     assert 0.9 < info["companion_fidelity"] <= 1.0
+
+
+@pytest.mark.parametrize("log2_tmax,method", [(12, 2), (16, 2), (20, 1)])
+def test_gate_kernel_all_modes_match_statevector(T, oracle_built, cfg2, monkeypatch, log2_tmax, method):
+    """The tensor-core gate kernel (gate_tc.cuh) in all three modes -- rowless gate (0), gate per B row (1),
+    A-row groups with the members' B rows as gate columns (2) -- on config 2 with TNB_GATE_ANY=1, which sends
+    every structurally eligible step to it regardless of size (the production thresholds only pick the big
+    ones).  The sum over all slices equals the oracle's exact state."""
+    import json
+    from oracle import sv
+    c, circ, bits, om = cfg2
+    monkeypatch.setenv("TNB_GATE_ANY", "1")
+    ss = T.SparseState(circ, bits, om)
+    info = ss.plan(1 << log2_tmax, n_sliced=2 if method == 2 else 4, method=method, seed=1, time_budget_s=5.0)
+    monkeypatch.delenv("TNB_GATE_ANY")
+    import tempfile, os
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "dump.json")
+        ss.dump(p)
+        modes = {s["gate_tc"] for s in json.load(open(p))["steps"] if "gate_tc" in s}
+    assert {0, 2} <= modes, modes
+    if log2_tmax == 16:
+        assert 1 in modes, modes
+    ss.bind(0, pipelines=2)
+    amps = ss.contract(range(1 << info["s"])).cpu().numpy()
+    want, _ = sv.amplitudes(circ, bits)
+    assert_amps_close(amps, want)
