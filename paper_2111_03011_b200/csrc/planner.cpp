@@ -1329,7 +1329,7 @@ std::string sweep_plan(const Network& net, const std::vector<Leaf>& leaves, cons
     for (int e = 0; e < (int)best_sliced.size(); e++)
         if (best_sliced[e] == 1) Sall.set(e);
     const double t_before = eval_tree(t, Sall).time;
-    {
+    if (!(getenv("TNB_NO_MERGE") && atoi(getenv("TNB_NO_MERGE")) != 0)) {
         Ctx cx{&rm, Sall, opt.max_elems};
         reconfigure(t, cx, elapsed() + std::max(2.0, 0.25 * budget), t0);
     }
