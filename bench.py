@@ -35,8 +35,8 @@ os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 from tn_inputs import configs  # noqa: E402
 
 METRIC = "slices/sec & complex TFLOP/s (frac of peak) at 1/2/4/8 B200; time to 1e6 amplitudes"
-DEFAULT_BLOCK = {4: 4, 3: 256}       # global slices per rank per step
-DEFAULT_PIPES = {4: 1, 3: 16}
+DEFAULT_BLOCK = {5: 2, 4: 4, 3: 256}  # global slices per rank per step
+DEFAULT_PIPES = {5: 1, 4: 1, 3: 16}
 
 
 def peaks():
@@ -283,7 +283,7 @@ def measure(args, T, torch, dist, dev, stream, cfg, rank, world, flush):
     loop = info["s_local"] > 0 or info["n_segments"] > 1
     if cfg.cfg >= 4:
         # weak scaling over global slices: rank r contracts its own block of B consecutive slices per step
-        B = min(args.block or DEFAULT_BLOCK[4], nS // world)
+        B = min(args.block or DEFAULT_BLOCK.get(cfg.cfg, 4), nS // world)
         block = list(range(rank * B, (rank + 1) * B))
         scaling = "weak"
         per_step_slices = B * world

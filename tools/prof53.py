@@ -34,3 +34,33 @@ for wms, i, w, p in rows[:40]:
     print(f"{wms:9.2f} ms ({100 * wms / tot:5.1f} %, cum {100 * acc / tot:5.1f} %) launch {i:3d} x{w}: {p['kind']:12s} "
           f"step {p['step']:3d} seg {p['seg']} ms {p['ms']:.3f} m {p['m']} n {p['n']} k {p['k']} rows {p['rows']} "
           f"GB {p['bytes'] / 1e9:.2f} GCMAC {p['cmac'] / 1e9:.2f} -> {p['bytes'] / p['ms'] / 1e6:.0f} GB/s", flush=True)
+
+# whole-run and fidelity-prefix extrapolation from the measured per-run segment times (one profiled pass):
+# segment j runs 2^|D_j| times over all global slices; over the prefix [0, 2^p) of global slice ids (fidelity
+# ~ 2^p / 2^s, PAPER.md L77 / L152) it runs 2^|D_j n (local bits u last p global bits)| times
+import json  # noqa: E402
+import math  # noqa: E402
+import tempfile  # noqa: E402
+
+with tempfile.NamedTemporaryFile(suffix=".json", delete=False) as f:
+    pth = f.name
+ss.save_plan(pth)
+pf = json.load(open(pth))
+os.unlink(pth)
+ns = len(pf["sliced"])
+glob = [i for i in range(ns) if pf["global"][i]]
+local = [i for i in range(ns) if not pf["global"][i]]
+seg_ms = {}
+for p in prof:
+    seg_ms[p["seg"]] = seg_ms.get(p["seg"], 0.0) + p["ms"]
+bit = lambda r: 1 << (ns - 1 - r)  # noqa: E731
+full = sum(seg_ms.get(j, 0.0) * 2.0 ** bin(int(D)).count("1") for j, (D, _, _) in enumerate(pf["segs"]))
+print(f"extrapolated whole run (all 2^{len(glob)} global slices, one GPU, serial profile): {full / 1e3:.4g} s")
+for F in (0.002, 0.0037):
+    pbits = max(0, min(len(glob), math.ceil(math.log2(F * 2 ** len(glob)))))
+    free = 0
+    for r in local + glob[len(glob) - pbits:]:
+        free |= bit(r)
+    t = sum(seg_ms.get(j, 0.0) * 2.0 ** bin(int(D) & free).count("1") for j, (D, _, _) in enumerate(pf["segs"]))
+    print(f"F ~ {F}: prefix of 2^{pbits} global slices (fraction {2 ** pbits / 2 ** len(glob):.4g}): {t / 1e3:.4g} s "
+          f"on one GPU; {t / 8e3:.4g} s on 8 (weak scaling over slices)")
