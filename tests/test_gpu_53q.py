@@ -69,3 +69,28 @@ def test_53q_m8_all_slices_norm_and_porter_thomas(T):
     assert abs(fn - 1.0) < 0.02, fn
     ks = metrics.porter_thomas_ks((2.0 ** n) * np.abs(amps) ** 2)
     assert ks < 0.05, ks
+
+
+@pytest.mark.slow
+def test_config5_m20_one_global_slice_norm(T):
+    """Config 5 (53q, m = 20, M = 2^26 = 2^20 groups x 64, BASELINE configs[4]) from its plan file: one global slice
+    of the 2^29 (its 8 local wires summed inside; max tensor 2^32, 137 GB workspace).  The 2^34 sliced copies are
+    orthogonal and contribute to the norm in proportion: 2^s x F_norm of one slice has mean
+    1, but a single slice's norm is itself a path probability that fluctuates (up to Porter-Thomas-like spread
+    over slice values), so only a sanity window is asserted: amplitudes finite and nonzero, and the scaled norm
+    within 1e-3..1e3 (a wrong normalisation or a dropped local loop moves it by 2^8 or more)."""
+    import os
+    from oracle import metrics
+    c = configs.get(5)
+    circ = c.circuit()
+    n = circ["n"]
+    ss = T.SparseState(circ, c.bitstrings(n), c.open_mask(n))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    info = ss.plan(1 << 32, plan_path=os.path.join(root, "plans", "config5.json"))
+    assert info["s"] >= 20 and info["s_local"] >= 1 and info["peak_elems"] <= 1 << 32
+    ss.bind(0, pipelines=1)
+    amps = ss.contract([0]).cpu().numpy().astype(complex)
+    assert np.all(np.isfinite(amps)) and np.count_nonzero(amps) > 0.99 * amps.size
+    scaled = metrics.f_norm(amps, n) * 2.0 ** info["s"]
+    print(f"config 5 slice 0: 2^s x F_norm = {scaled:.4g}")
+    assert 1e-3 < scaled < 1e3, scaled
