@@ -367,3 +367,24 @@ def test_companion_truncation_matches_oracle(T, oracle_built):
         want = sv.sliced_amplitudes(circ, bits, wires, subset, companions=comps)
         assert_amps_close(ss.contract(subset).cpu().numpy(), want)
     assert 0.9 < info["companion_fidelity"] <= 1.0
+
+
+def test_more_slices_than_one_id_upload(T, oracle_built):
+    """2^13 slices on one pipeline: more than the 4096 slice ids one upload holds (the captured graph keeps the id
+    buffer's address, so tn_contract feeds longer blocks in chunks -- round-1 ADVICE).  All slices summed = the exact
+    state; the first 6144 slices = Pi_0 on wire 0 plus (Pi_1 on wire 0, Pi_0 on wire 1) -- two oracle runs."""
+    from oracle import sv
+    c = configs.get(2)
+    circ = c.circuit()
+    n = circ["n"]
+    bits = c.bitstrings(n)
+    ss = T.SparseState(circ, bits, c.open_mask(n))
+    info = ss.plan(1 << 20, n_sliced=13, method=1, seed=1, time_budget_s=5.0)
+    assert info["s"] == 13
+    ss.bind(0, pipelines=1)
+    want, _ = sv.amplitudes(circ, bits)
+    assert_amps_close(ss.contract(range(1 << 13)).cpu().numpy(), want)
+    W = info["sliced_wires"]
+    a0, _ = sv.amplitudes(circ, bits, [(W[0][0], W[0][1], 0)])
+    a1, _ = sv.amplitudes(circ, bits, [(W[0][0], W[0][1], 1), (W[1][0], W[1][1], 0)])
+    assert_amps_close(ss.contract(range(6144)).cpu().numpy(), a0 + a1)
