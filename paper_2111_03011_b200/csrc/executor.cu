@@ -1297,7 +1297,11 @@ int build_pipe(Device* d, Pipe& P, const std::vector<Step>& steps, std::string& 
                 }
                 L.gC = (float*)ptr(g.C);
                 L.gN2 = g.embed_a ? g.n : 2 * g.n;
-                L.gEA = g.embed_a;
+                L.gEA = g.embed_a | (g.c_colmajor << 1);  // bit 1: column-major C (gemm_tc.cuh plain epilogue)
+                if (g.c_colmajor) {
+                    L.gCm = g.m;
+                    L.gCn = g.n;
+                }
                 if (g.grouped) {
                     L.gTiles = (const int4*)ptr(L.gCG == 2 ? g.tiles2 : g.tiles);
                     L.gPerm = (const int32_t*)ptr(g.perm);

@@ -183,7 +183,7 @@ template <int BN, int CG = 1, bool GA = false>
 __global__ void __launch_bounds__(GA ? THREADS + GA_PROD : THREADS, 1)
     k_gemm_tf32x3(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                   const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
-                  float* __restrict__ C, int64_t Mp, int64_t N2, int64_t K2, int ea,
+                  float* __restrict__ C, int64_t Mp, int64_t N2, int64_t K2, int ea_flags,
                   const int4* __restrict__ tiles, const int32_t* __restrict__ perm, int64_t cm, int64_t cn,
                   int n_tiles, int tiles_n, const GatherA ga) {
     using CF = Cfg<BN, CG>;
@@ -213,6 +213,8 @@ __global__ void __launch_bounds__(GA ? THREADS + GA_PROD : THREADS, 1)
     const int tile0 = (int)blockIdx.x / CG, tstride = (int)gridDim.x / CG;
     // grouped scatter: cm (rows per output row-block) and cn (columns) are powers of two
     const int lcm = 63 - __clzll(cm > 0 ? cm : 1), lcn = 63 - __clzll(cn > 0 ? cn : 1);
+    const int ea = ea_flags & 1;            // embedded A
+    const bool cmaj = (ea_flags & 2) != 0;  // plain C stored column-major within a row: (r, n, m) with m lowest
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
@@ -525,6 +527,18 @@ __global__ void __launch_bounds__(GA ? THREADS + GA_PROD : THREADS, 1)
                                 *(float2*)(C + 2 * ((((r << lcm) + fa) << lcn) + fb)) = make_float2(re, im);
                             }
                         }
+                    }
+                } else if (!ea && cmaj) {
+                    // column-major C (lower.cpp): complex (m = gm, n) at ((r << lcn) + n) << lcm | orbit, r = gm >> lcm;
+                    // the 32 lanes hold consecutive m, so each store is 256 contiguous bytes
+                    if (gm < Mp) {
+                        float2* C2 = (float2*)C;
+                        const int64_t rb = ((gm >> lcm) << (lcm + lcn)) + (gm & (cm - 1));
+                        const int64_t nf = (int64_t)(n0 + c0) >> 1;
+#pragma unroll
+                        for (int q = 0; q < 16; q++)
+                            if (nf + q < cn)
+                                C2[rb + ((nf + q) << lcm)] = make_float2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
                     }
                 } else if (!ea) {
                     // D = C interleaved: row gm of D is row gm of C (real columns 2n, 2n+1 = re, im)

@@ -610,6 +610,16 @@ std::string lower_plan(const Network& net, const std::vector<Leaf>& leaves, cons
             } else {
                 // embed the smaller operand in the complex-as-real GEMM (its rows double); EA needs n >= 32
                 gp.embed_a = ((Mp < n && n >= 128) || Mp < 128) && n >= 32 ? 1 : 0;
+                // plain GEMM, opt-in TNB_GEMM_CMAJ=1: store C column-major within each row (B-free legs on top,
+                // A-free legs low), so that the epilogue's lanes (consecutive m) write consecutive addresses.
+                // Measured (same box): config-4 k=64 n=256 GEMM 4.06 -> 3.50 ms but the step total unchanged,
+                // config 3 -3 % (its consumers prefer the row-major result), so the default stays row-major
+                static const bool cmaj_on = getenv("TNB_GEMM_CMAJ") && atoi(getenv("TNB_GEMM_CMAJ")) != 0;
+                if (!gp.embed_a && cmaj_on && m >= 32) {
+                    gp.c_colmajor = 1;
+                    Cn.legs = fb;
+                    Cn.legs.insert(Cn.legs.end(), fa.begin(), fa.end());
+                }
             }
             const int64_t abytes = (gp.embed_a ? 2 : 1) * Mp * 2 * k * 4,
                           bbytes = (gp.embed_a ? 1 : 2) * NBcols * 2 * k * 4;

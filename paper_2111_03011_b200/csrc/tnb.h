@@ -244,6 +244,7 @@ struct GemmParams {
     BitMap aM, aK;            // A index bits from (m index bit -> A bit), (k index bit -> A bit)
     BitMap bN, bK;            // B index bits from (n index bit -> B bit), (k index bit -> B bit)
     int gather_a = 0;         // 1: no A pre-pass; the GEMM's producer warps gather + split A (gemm_tc.cuh GatherA)
+    int c_colmajor = 0;       // plain GEMM: C legs = B-free legs on top, A-free legs low (coalesced epilogue stores)
     int embed_a = 0;          // 1: embed A ([2Mp][2K] rows (ar,-ai),(ai,ar)), B plain [N][2K] ("EA");
                               // 0: A plain [Mp][2K], embed B ([2N][2K] rows (br,-bi),(bi,br)) ("EB")
     // grouped mode (both operands carry rows, SURVEY a6 GATHER-CONTRACT on the tensor cores): output
