@@ -35,7 +35,7 @@ os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 from tn_inputs import configs  # noqa: E402
 
 METRIC = "slices/sec & complex TFLOP/s (frac of peak) at 1/2/4/8 B200; time to 1e6 amplitudes"
-DEFAULT_BLOCK = {5: 2, 4: 4, 3: 256}  # global slices per rank per step
+DEFAULT_BLOCK = {5: 2, 4: 8, 3: 256}  # global slices per rank per step (config 4: 8 = the steady-state segment-run ratio)
 DEFAULT_PIPES = {5: 1, 4: 1, 3: 16}
 
 
